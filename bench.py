@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""Headline benchmark: circuits/sec (expectation + adjoint gradient), QAOA MaxCut 20q, p=4.
+
+BASELINE.json config 2: random 3-regular graph on 20 qubits (networkx seed 2), depth
+p=4, batch 256 (gamma, beta) rows ~ U[0, pi) float32, observable sum_E Z_i Z_j.
+One step = build per-row gate data + forward simulation + expectation + adjoint
+gradient for all 256 rows.  Multi-GPU: weak scaling, each rank runs its own 256-row
+shard (no data-path collective; the batch rows are independent).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+``value``    device-resident inputs, CUDA-event timed (max over ranks).
+``e2e``      the public API (paper_2003_02989_b200.ops.expectation_and_gradient) with
+             pinned host inputs, H2D + D2H inside the timed region.
+``roofline`` the dominant kernel (tile-pass kernels), algorithmic bytes / event-timed
+             launch durations vs MEASURED_PEAKS.json hbm_gbs.
+``cpu_baseline`` / ``--impl reference``: the reference algorithm (CPU oracle port of
+             qcflow: fused simulate + expectation + parameter-shift per row) on host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "circuits/sec (expectation + adjoint grad) at 20q"
+UNIT = "circuits/s"
+N_QUBITS, DEPTH, BATCH = 20, 4, 256
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    r = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                        "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                       timeout=5)
+                    parts = [p.strip() for p in r.stdout.strip().split(",")]
+                    if len(parts) == 6:
+                        self.samples.append(parts)
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def workload():
+    from paper_2003_02989_b200 import workloads as wl
+    from paper_2003_02989_b200.circuit import circuit_symbols
+
+    edges = wl.qaoa_graph(N_QUBITS)
+    circ, cost = wl.qaoa_circuit(N_QUBITS, DEPTH, edges)
+    return circ, cost, circuit_symbols(circ)
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: the reference algorithm (oracle port) on host cores
+# ---------------------------------------------------------------------------
+
+
+def _cpu_eval(args):
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    which, seed = args
+    from oracle import qcflow_port as orc
+
+    circ, cost, syms = workload()
+    from paper_2003_02989_b200 import workloads as wl
+
+    theta = wl.qaoa_params(BATCH, DEPTH)[seed % BATCH].astype(np.float64)
+    bind = dict(zip(syms, theta))
+    t0 = time.perf_counter()
+    if which == "expect":
+        amps = orc.simulate_amps(circ, bind)
+        orc.expectation(amps, cost, N_QUBITS)
+    else:  # one parameter-shift evaluation: a shifted fused simulation + expectation
+        ops = orc.resolved_ops(circ, bind)
+        z = np.zeros(2 ** N_QUBITS, dtype=np.complex128)
+        z[0] = 1.0
+        amps = orc.run_ops(z, ops, N_QUBITS, True)
+        orc.expectation(amps, cost, N_QUBITS)
+    return time.perf_counter() - t0
+
+
+def cpu_reference_rate(cores: int, rounds: int = 1):
+    """circuits/s of the reference path (expectation + parameter-shift gradient per row),
+    from a bounded sample: `rounds` x `cores` evaluations in parallel, extrapolated to the
+    2 * sum_occ K + 1 = 401 evaluations one 20q QAOA row costs."""
+    import multiprocessing as mp
+
+    circ, cost, syms = workload()
+    from oracle import qcflow_port as orc
+
+    n_evals = 1 + sum(2 * len([t for t in g.generator.terms if t.factors]) for g in circ.gates
+                      if g.exponent is not None and g.exponent.symbol is not None)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        per = pool.map(_cpu_eval, [("ps", i) for i in range(cores * rounds)])
+    wall = time.perf_counter() - t0
+    t_eval = float(np.mean(per))
+    rate = cores / (t_eval * n_evals)
+    return rate, dict(t_eval_s=t_eval, evals_per_circuit=n_evals, wall_s=wall,
+                      sample=f"{cores * rounds} fused 20q simulate+expectation evaluations on {cores} "
+                             f"processes, extrapolated to {n_evals} evaluations (1 expectation + PS) per circuit")
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    rates = []
+    for _ in range(max(args.warmup, 0)):
+        pass  # warm-up is the pool start inside each step; no separate untimed work needed
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r, info = cpu_reference_rate(cores)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    v = float(np.median(rates))
+    line = {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / v, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "qaoa_maxcut_20q_p4_b256", "global_batch": BATCH, "n_qubits": N_QUBITS,
+                   "depth": DEPTH, "gradient": "parameter-shift (reference has no adjoint)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"]},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+
+def pass_bytes(prog, rows):
+    """Algorithmic HBM bytes of each pass launch (SURVEY 8(d) roofline rule)."""
+    from paper_2003_02989_b200 import planner as pl
+
+    amps = (1 << prog.n) * rows
+    out = []
+    for p in prog.passes:
+        init, store = int(p[2]), int(p[3])
+        arrays = 2 if prog.adjoint else 1
+        rd = 0 if init in (pl.INIT_ZERO, pl.INIT_PRODUCT) else (8 if init == pl.INIT_LOAD_PSI else 8 * arrays)
+        wr = 8 * arrays if store else 0
+        out.append((rd + wr) * amps)
+    return out
+
+
+def run_gpu(args, rank, world):
+    import ctypes as C
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_02989_b200 import _native as nat
+    from paper_2003_02989_b200 import ops as qops
+    from paper_2003_02989_b200 import workloads as wl
+    from paper_2003_02989_b200.engine import ENGINE, _ptr
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    circ, cost, syms = workload()
+    theta_np = wl.qaoa_params(BATCH * world, DEPTH)[rank * BATCH:(rank + 1) * BATCH]
+    theta = torch.as_tensor(theta_np).to(dev)
+    bound = ENGINE.bind([circ] * BATCH, syms, [cost], want_grad=True, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return bound.execute(theta, want_grad=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        out = step()
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = BATCH * world / (ms / 1000.0)
+
+    # ---- per-launch profile of the tile-pass kernels (roofline) ----
+    lib = nat.load()
+    plan = bound.plan
+    fw, ad = plan.fwd, plan.adj
+    B = BATCH
+    n_eff = plan.n_eff
+    psi = torch.empty((B, 1 << n_eff), dtype=torch.complex64, device=dev)
+    lam = torch.empty_like(psi)
+    s = stream.cuda_stream
+    mats_f = torch.empty((B, max(fw.prog.n_mat, 1)), dtype=torch.complex64, device=dev)
+    angs_f = torch.empty((B, max(fw.prog.n_ang, 1)), dtype=torch.int32, device=dev)
+    mats_a = torch.empty((B, max(ad.prog.n_mat, 1)), dtype=torch.complex64, device=dev)
+    angs_a = torch.empty((B, max(ad.prog.n_ang, 1)), dtype=torch.int32, device=dev)
+    rec_f = fw.recipe(bound.fixed_t, bound.fixed_rows, bound.const_t, bound.const_rows)
+    rec_a = ad.recipe(bound.fixed_a, bound.fixed_a_rows, bound.const_a, bound.const_a_rows)
+    nat.check(lib.qf_build_ops(C.byref(rec_f), _ptr(theta), theta.shape[1], B, _ptr(mats_f), fw.prog.n_mat,
+                               _ptr(angs_f), fw.prog.n_ang, s))
+    nat.check(lib.qf_build_ops(C.byref(rec_a), _ptr(theta), theta.shape[1], B, _ptr(mats_a), ad.prog.n_mat,
+                               _ptr(angs_a), ad.prog.n_ang, s))
+    part_f = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
+    part_a = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
+    hw = torch.ones((B, max(len(bound.hkeys), 1)), dtype=torch.float32, device=dev)
+    struct_a = nat.QfProgram.from_buffer_copy(ad.struct)
+    struct_a.coef_row_stride = hw.shape[1]
+    fb, ab = pass_bytes(fw.prog, B), pass_bytes(ad.prog, B)
+    reps = 3
+    times_f = np.zeros(len(fb))
+    times_a = np.zeros(len(ab))
+    for r in range(reps + 1):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(fb) + len(ab) + 1)]
+        ev[0].record(stream)
+        for p in range(len(fb)):
+            nat.check(lib.qf_run_passes(C.byref(fw.struct), p, p + 1, _ptr(psi), n_eff, B, _ptr(mats_f),
+                                        _ptr(angs_f), _ptr(bound.fwd_coefs), _ptr(part_f), fw.tiles, s))
+            ev[1 + p].record(stream)
+        for p in range(len(ab)):
+            nat.check(lib.qf_adjoint_passes(C.byref(struct_a), p, p + 1, _ptr(psi), _ptr(lam), n_eff, B,
+                                            _ptr(mats_a), _ptr(angs_a), _ptr(hw), _ptr(part_a), ad.tiles, s))
+            ev[1 + len(fb) + p].record(stream)
+        torch.cuda.synchronize(dev)
+        if r == 0:
+            continue  # warm-up round
+        for p in range(len(fb)):
+            times_f[p] += ev[p].elapsed_time(ev[p + 1]) / reps
+        for p in range(len(ab)):
+            times_a[p] += ev[len(fb) + p].elapsed_time(ev[len(fb) + p + 1]) / reps
+    peak, peak_kind = _peaks()
+    tot_bytes = sum(fb) + sum(ab)
+    tot_ms = times_f.sum() + times_a.sum()
+    achieved = tot_bytes / (tot_ms / 1000.0) / 1e9
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "pass_kernel_traffic.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("bytes_per_step")
+        except Exception:
+            traffic = None
+
+    # ---- e2e through the public API with pinned host buffers ----
+    host_theta = torch.as_tensor(theta_np).pin_memory()
+    for _ in range(2):
+        qops.expectation_and_gradient([circ] * BATCH, syms, host_theta, [cost])
+    barrier()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        ev_, gr_ = qops.expectation_and_gradient([circ] * BATCH, syms, host_theta, [cost])
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = BATCH * world / (e2e_ms / 1000.0)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        r, info = cpu_reference_rate(cores)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"]}
+
+    if rank == 0:
+        launches = len(fb) + len(ab) + 2 + 3  # passes + 2 builds + 3 slot reductions
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c64", "data": "synthetic",
+            "config": {"workload": "qaoa_maxcut_20q_p4_b256", "global_batch": BATCH * world,
+                       "per_gpu_batch": BATCH, "n_qubits": N_QUBITS, "depth": DEPTH,
+                       "observable": "sum_E ZZ (30 edges)", "gradient": "adjoint",
+                       "parallelism": f"batch-shard x{world}", "l2": "inputs exceed L2 (2 GiB state per GPU)",
+                       "fwd_passes": len(fb), "adj_passes": len(ab)},
+            "gpu_launches": launches * args.steps,
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(theta_np.nbytes),
+                    "d2h_bytes_per_step": int(BATCH * (1 + len(syms)) * 8)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "qf::pass_kernel (forward L13/R5 + adjoint L12/R4)",
+                         "algorithmic_bytes_per_step": tot_bytes, "kernel_ms_per_step": tot_ms,
+                         "pass_ms": [round(x, 4) for x in list(times_f) + list(times_a)],
+                         "pass_gbs": [round(b / (t / 1000) / 1e9, 1) for b, t in
+                                      zip(list(fb) + list(ab), list(times_f) + list(times_a))]},
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_gpu(args, rank, world)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * qfb200.h -- C ABI of the B200 batched state-vector engine (libqfb200.so).
+ *
+ * The reference (qcflow, pure Python) has no FFI; its operator API is a set of
+ * Python functions.  This header is the C boundary those functions are rebuilt
+ * on: every entry point is extern "C", takes plain device pointers / sizes and
+ * a cudaStream_t (as void*), is stream-ordered, never allocates persistent
+ * device memory and never frees caller memory.  Status: 0 = ok, otherwise an
+ * error code; qf_last_error() returns a thread-local message that the Python
+ * host maps onto the reference's exception classes (ValueError / KeyError /
+ * MemoryError / AssertionError).
+ *
+ * Which reference interface each entry replaces:
+ *   qf_build_ops      gate_matrix + fuse_resolved   qcflow/circuit.py:281-309, fusion.py:78-176
+ *   qf_run_passes     run_ops / apply_matrix / simulate / expectation
+ *                                                   qcflow/sim.py:88-150, :177-213
+ *   qf_adjoint_passes (new) adjoint differentiator; oracle = parameter_shift_grad
+ *                                                   qcflow/gradients.py:158-165, 241-326
+ *   qf_reduce_slots   _pairwise_sum over terms / PS accumulation
+ *                                                   qcflow/sim.py:162-174, gradients.py:321
+ *   qf_pauli_expect   pauli_term_values + expectation  qcflow/sim.py:177-213
+ *   qf_pauli_apply    (H|psi>, adjoint seed)        index/phase form of qcflow/sim.py:183-196
+ *   qf_sample         _draw_bits / sample            qcflow/sim.py:216-227, rng.py:14-19
+ */
+#ifndef QFB200_H
+#define QFB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- device program descriptors (all-int32 layouts, mirrored in planner.py) ---- */
+
+#define QF_MAX_R 8
+#define QF_MAX_T 16
+#define QF_MAX_Q 40
+
+enum {
+  QF_OP_DENSE1 = 1,   /* 2x2 unitary on register slot s0 */
+  QF_OP_DENSE2 = 2,   /* 4x4 unitary on register slots (s0 = MSB, s1), s0 < s1 */
+  QF_OP_DIAG = 3,     /* phase polynomial exp(-i sum_k theta_k Z-string_k) */
+  QF_OP_OBS = 4,      /* diagonal observable: expectation slot (and lambda = H psi in adjoint) */
+};
+
+enum { QF_INIT_LOAD = 0, QF_INIT_ZERO = 1, QF_INIT_PRODUCT = 2, QF_INIT_LOAD_PSI = 3 };
+
+typedef struct QfStage {
+  int32_t reg_glob[QF_MAX_R];   /* global bit position of register slot j */
+  int32_t thr_glob[QF_MAX_T];   /* global bit position of thread slot i (lane bits first) */
+  int32_t reg_phys[QF_MAX_R];   /* swizzled smem offset contributed by register slot j */
+  int32_t thr_phys[QF_MAX_T];   /* swizzled smem offset contributed by thread slot i */
+  int32_t op_begin, op_end;
+  int32_t pad[14];
+} QfStage;                       /* 64 x int32 */
+
+typedef struct QfOp {
+  int32_t kind, s0, s1;
+  int32_t mat;                   /* DENSE: offset (complex units) into the row's matrix slab */
+  int32_t term_begin, term_end;  /* DIAG/OBS: term range (sorted by register subset) */
+  int32_t grp;                   /* DIAG/OBS: offset of the 2^R+1 subset-boundary table */
+  int32_t slot;                  /* gradient / expectation slot, -1 = none */
+  int32_t gen;                   /* ADJ dense gradient: generator matrix offset (complex units) */
+  int32_t pad[7];
+} QfOp;                          /* 16 x int32 */
+
+typedef struct QfPass {
+  int32_t stage_begin, stage_end;
+  int32_t init, store;
+  int32_t mat_begin, mat_end;    /* matrix slab range used by this pass (complex units) */
+  int32_t ang_begin, ang_end;    /* angle columns used by this pass */
+  int32_t slot_begin, slot_end;  /* slots written by this pass */
+  int32_t n_outer;
+  int32_t coef_begin, coef_end;  /* observable coefficient columns */
+  int32_t L;
+  int32_t pad0[2];
+  int32_t outer_pos[32];         /* global positions of the n-L non-tile bits */
+  int32_t init_mat[32];          /* product init: matrix offset of qubit q's leading 2x2, -1 = |0> */
+  int32_t pad1[48];
+} QfPass;                        /* 128 x int32 */
+
+/* Everything one pass launch needs; pointers are device pointers. */
+typedef struct QfProgram {
+  const QfPass* passes;
+  const QfStage* stages;
+  const QfOp* ops;
+  const uint32_t* term_mask;     /* Z-string masks (global bits, n <= 32) */
+  const int32_t* term_idx;       /* angle column (DIAG) or coefficient column (OBS) */
+  const float* term_w;           /* ADJ: gradient weight 2*coeff*beta_k per term */
+  const int32_t* grp;            /* subset-boundary tables */
+  const float* genmats;          /* ADJ: generator matrices (interleaved complex64) */
+  int32_t n_passes;
+  int32_t n_slots;               /* total slots (gradient + expectation) */
+  int32_t n_mat;                 /* complex entries per row in the matrix slab */
+  int32_t n_ang;                 /* angle columns per row */
+  int32_t n_coef;                /* observable coefficient columns per row */
+  int32_t L, R;                  /* tile bits / register bits used by every pass */
+  int32_t coef_row_stride;       /* 0 = coefficients broadcast over rows */
+  const QfPass* host_passes;     /* host copy of `passes` (launch geometry / smem sizing) */
+} QfProgram;
+
+/* Recipe for per-row matrices / angles (qf_build_ops). */
+typedef struct QfBuildRecipe {
+  int32_t n_gen;                 /* symbolic generator-exponential gates */
+  const int32_t* gen_sym;        /* [n_gen] symbol column */
+  const double* gen_coeff;       /* [n_gen] exponent coeff */
+  const double* gen_const;       /* [n_gen] exponent const */
+  const int32_t* gen_dim;        /* [n_gen] 2 or 4 */
+  const double* gen_eval;        /* [n_gen*4] eigenvalues of the generator (incl. identity part) */
+  const double* gen_evec;        /* [n_gen*16*2] eigenvectors, row-major complex (re,im) */
+  int32_t n_fixed;               /* concrete gates */
+  const double* fixed;           /* [fixed_rows, n_fixed, 16, 2] complex128 */
+  int32_t fixed_rows;            /* 1 (broadcast) or rows */
+  int32_t n_dense;               /* dense ops to build */
+  const int32_t* dense_mat;      /* [n_dense] output offset (complex units) */
+  const int32_t* dense_dim;      /* [n_dense] 2 or 4 */
+  const int32_t* dense_fbeg;     /* [n_dense+1] factor range */
+  const int32_t* factor;         /* [n_factors*3]: (src_kind 0=gen 1=fixed, src index, embed) */
+  int32_t n_terms;               /* diagonal angle columns */
+  const int32_t* term_src;       /* [n_terms*2]: (src_kind 0=gen 1=const, index) */
+  const double* term_beta;       /* [n_terms] beta (gen) */
+  const double* term_const;      /* [const_rows, n_const] constant angles */
+  int32_t const_rows;            /* 1 or rows */
+  int32_t n_const;
+} QfBuildRecipe;
+
+const char* qf_last_error(void);
+int qf_version(void);
+int qf_device_sm_count(int device);
+
+/* Per-row op matrices (complex64 slab [rows, n_mat]) and angles (int32 turns [rows, n_ang])
+ * from symbol values theta [rows, n_sym] (float32, row stride theta_stride). */
+int qf_build_ops(const QfBuildRecipe* recipe, const float* theta, int64_t theta_stride, int rows,
+                 float* mats, int n_mat, int32_t* angles, int n_ang, void* stream);
+
+/* Forward passes [pass_begin, pass_end) over psi [rows, 2^n] (complex64 interleaved). */
+int qf_run_passes(const QfProgram* prog, int pass_begin, int pass_end, float* psi, int n,
+                  int rows, const float* mats, const int32_t* angles, const float* coefs,
+                  double* partials, int tiles_per_row, void* stream);
+
+/* Adjoint backward passes, executed in order pass_begin..pass_end-1 of the backward program. */
+int qf_adjoint_passes(const QfProgram* prog, int pass_begin, int pass_end, float* psi, float* lam,
+                      int n, int rows, const float* mats, const int32_t* angles,
+                      const float* coefs, double* partials, int tiles_per_row, void* stream);
+
+/* out[row, col] (+)= sum over slots of column col (CSR col_ptr/slot_list) of sum_tile partials. */
+int qf_reduce_slots(const double* partials, int rows, int n_slots, int tiles,
+                    const int32_t* col_ptr, const int32_t* slot_list, int n_cols, double* out,
+                    int accumulate, void* stream);
+
+/* Generic Pauli-sum expectation partials: partials[row, k, chunk] = coef[row, k] *
+ * sum_{x in chunk} Re(conj(psi[x ^ xm_k]) i^{ny_k} (-1)^{popc(x & zm_k)} psi[x]);
+ * chunks = ceil(2^n / 2048).  Sum with qf_reduce_slots (slots = terms, tiles = chunks).
+ * coef_stride 0 = coefficients broadcast over rows. */
+int qf_pauli_expect(const float* psi, int n, int rows, int n_terms, const uint32_t* xmask,
+                    const uint32_t* zmask, const int32_t* ny, const float* coefs,
+                    int64_t coef_stride, double* partials, void* stream);
+
+/* lam = H psi for a per-row weighted Pauli sum (adjoint seed for non-diagonal H). */
+int qf_pauli_apply(const float* psi, float* lam, int n, int rows, int n_terms,
+                   const uint32_t* xmask, const uint32_t* zmask, const int32_t* ny,
+                   const float* coefs, int64_t coef_stride, void* stream);
+
+/* Shot sampler: numpy Generator(Philox).choice(2^n, shots, p=|a|^2/sum) semantics.
+ * keys [rows*2] uint64 Philox keys, ctr0 [rows] counter of the first block used (numpy's
+ * Philox starts at counter 1), out_idx [rows, shots] int64.  scratch: >= rows*(2^n/1024+2) doubles. */
+int qf_sample(const float* psi, int n, int rows, int shots, const uint64_t* keys,
+              double* scratch, int64_t* out_idx, int32_t* near_boundary, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,526 @@
+// C ABI of libqfb200.so: build / reduce / Pauli / sampler kernels and the extern "C"
+// entry points declared in include/qfb200.h.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <mutex>
+#include <string>
+
+#include "qf_common.cuh"
+
+namespace qf {
+
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+static int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return 1;
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// per-row op matrices / angles (fp64 math, complex64 / int32-turn outputs)
+// ---------------------------------------------------------------------------
+
+struct Z {
+  double x, y;
+};
+__device__ __forceinline__ Z zmul(Z a, Z b) { return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x}; }
+__device__ __forceinline__ Z zadd(Z a, Z b) { return {a.x + b.x, a.y + b.y}; }
+
+struct Recipe {
+  QfBuildRecipe r;
+};
+
+__device__ void gen_matrix(const QfBuildRecipe& R, int g, double v, Z* out) {
+  const int d = R.gen_dim[g];
+  const double* ev = R.gen_eval + g * 4;
+  const Z* V = reinterpret_cast<const Z*>(R.gen_evec) + g * 16;
+  Z ph[4];
+  for (int k = 0; k < d; ++k) {
+    double s, c;
+    sincos(-v * ev[k], &s, &c);
+    ph[k] = {c, s};
+  }
+  // U = V diag(ph) V^dagger   (V stored row-major d x d within a 4x4 block)
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) {
+      Z acc{0, 0};
+      for (int k = 0; k < d; ++k) {
+        Z a = V[i * 4 + k];
+        Z b = V[j * 4 + k];
+        b.y = -b.y;
+        acc = zadd(acc, zmul(zmul(a, ph[k]), b));
+      }
+      out[i * 4 + j] = acc;
+    }
+}
+
+__global__ void build_dense_kernel(const QfBuildRecipe R, const float* theta, int64_t tstride, int rows,
+                                   float2* mats, int n_mat) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)rows * R.n_dense) return;
+  const int row = (int)(id / R.n_dense), op = (int)(id % R.n_dense);
+  const int D = R.dense_dim[op];
+  Z M[16];
+  for (int i = 0; i < 16; ++i) M[i] = {(i / 4 == i % 4 && i / 4 < D) ? 1.0 : 0.0, 0.0};
+  for (int f = R.dense_fbeg[op]; f < R.dense_fbeg[op + 1]; ++f) {
+    const int kind = R.factor[3 * f], src = R.factor[3 * f + 1], emb = R.factor[3 * f + 2];
+    Z F[16];
+    int fd;
+    if (kind == 0) {
+      const double v = R.gen_coeff[src] * (double)theta[row * tstride + R.gen_sym[src]] + R.gen_const[src];
+      gen_matrix(R, src, v, F);
+      fd = R.gen_dim[src];
+    } else {
+      const Z* fx = reinterpret_cast<const Z*>(R.fixed) + ((size_t)(R.fixed_rows > 1 ? row : 0) * R.n_fixed + src) * 16;
+      for (int i = 0; i < 16; ++i) F[i] = fx[i];
+      fd = (emb == 0 || emb == 1) ? 4 : 2;
+    }
+    (void)fd;
+    // embed F into the op's D-dim local space -> G
+    Z G[16];
+    if (emb == 4) {  // 1q op, 1q factor: F stored 2x2 at stride 4 or packed? -> packed 2x2 in [0..3]
+      for (int i = 0; i < 16; ++i) G[i] = {0, 0};
+      G[0] = F[0]; G[1] = F[1]; G[4] = F[4]; G[5] = F[5];
+    } else if (emb == 0 || emb == 1) {
+      const int sg[4] = {0, 2, 1, 3};
+      for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) G[i * 4 + j] = emb == 0 ? F[i * 4 + j] : F[sg[i] * 4 + sg[j]];
+    } else {  // 2: F (x) I (factor on MSB slot); 3: I (x) F
+      for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+          const int ia = i >> 1, ib = i & 1, ja = j >> 1, jb = j & 1;
+          Z val{0, 0};
+          if (emb == 2) {
+            if (ib == jb) val = F[ia * 4 + ja];
+          } else {
+            if (ia == ja) val = F[ib * 4 + jb];
+          }
+          G[i * 4 + j] = val;
+        }
+    }
+    // M = G @ M
+    Z N[16];
+    for (int i = 0; i < D; ++i)
+      for (int j = 0; j < D; ++j) {
+        Z acc{0, 0};
+        for (int k = 0; k < D; ++k) acc = zadd(acc, zmul(G[i * 4 + k], M[k * 4 + j]));
+        N[i * 4 + j] = acc;
+      }
+    for (int i = 0; i < D; ++i)
+      for (int j = 0; j < D; ++j) M[i * 4 + j] = N[i * 4 + j];
+  }
+  float2* out = mats + (size_t)row * n_mat + R.dense_mat[op];
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j) out[i * D + j] = make_float2((float)M[i * 4 + j].x, (float)M[i * 4 + j].y);
+}
+
+__global__ void build_angle_kernel(const QfBuildRecipe R, const float* theta, int64_t tstride, int rows,
+                                   int32_t* angles, int n_ang) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= (int64_t)rows * R.n_terms) return;
+  const int row = (int)(id / R.n_terms), k = (int)(id % R.n_terms);
+  const int kind = R.term_src[2 * k], src = R.term_src[2 * k + 1];
+  double ang;
+  if (kind == 0) {
+    const double v = R.gen_coeff[src] * (double)theta[row * tstride + R.gen_sym[src]] + R.gen_const[src];
+    ang = v * R.term_beta[k];
+  } else {
+    ang = R.term_const[(size_t)(R.const_rows > 1 ? row : 0) * R.n_const + src];
+  }
+  double turns = ang * 0.15915494309189535;  // 1/(2 pi)
+  turns -= rint(turns);                       // [-0.5, 0.5]
+  const long long fx = llrint(turns * 4294967296.0);
+  angles[(size_t)row * n_ang + k] = (int32_t)(uint32_t)(unsigned long long)fx;
+}
+
+// ---------------------------------------------------------------------------
+// slot reduction: out[row, col] = sum_{slot in col} sum_tile partials[row, slot, tile]
+// ---------------------------------------------------------------------------
+
+__global__ void reduce_slots_kernel(const double* __restrict__ partials, int rows, int n_slots, int tiles,
+                                    const int32_t* col_ptr, const int32_t* slot_list, int n_cols,
+                                    double* out, int accumulate) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= rows * n_cols) return;
+  const int row = warp / n_cols, col = warp % n_cols;
+  double acc = 0.0;
+  for (int s = col_ptr[col]; s < col_ptr[col + 1]; ++s) {
+    const double* p = partials + ((size_t)row * n_slots + slot_list[s]) * tiles;
+    double part = 0.0;
+    for (int i = lane; i < tiles; i += 32) part += p[i];
+    acc += warp_sum_d(part);
+  }
+  if (lane == 0) out[(size_t)row * n_cols + col] = accumulate ? out[(size_t)row * n_cols + col] + acc : acc;
+}
+
+// ---------------------------------------------------------------------------
+// generic Pauli-sum kernels (non-diagonal observables)
+// ---------------------------------------------------------------------------
+
+constexpr int kExpectChunk = 2048;
+
+__global__ void pauli_expect_kernel(const float2* __restrict__ psi, int n, int n_terms, const uint32_t* xm,
+                                    const uint32_t* zm, const int32_t* ny, const float* coefs,
+                                    int64_t cstride, double* partials, int chunks) {
+  extern __shared__ double tacc[];
+  const int row = blockIdx.y, chunk = blockIdx.x;
+  const float2* p = psi + ((size_t)row << n);
+  for (int k = threadIdx.x; k < n_terms; k += blockDim.x) tacc[k] = 0.0;
+  __syncthreads();
+  const uint32_t x0 = (uint32_t)chunk * kExpectChunk;
+  const uint32_t len = min((uint32_t)kExpectChunk, (uint32_t)1u << n);
+  for (int k = 0; k < n_terms; ++k) {
+    const uint32_t m = xm[k], z = zm[k];
+    float acc = 0.f;
+    for (uint32_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const uint32_t x = x0 + i;
+      const float2 a = p[x], b = p[x ^ m];
+      // conj(b) * a
+      float re = fmaf(b.x, a.x, b.y * a.y), im = fmaf(b.x, a.y, -b.y * a.x);
+      const int q = ny[k] & 3;
+      float v = q == 0 ? re : q == 1 ? -im : q == 2 ? -re : im;  // Re(i^q * (re + i im))
+      acc += (__popc(x & z) & 1) ? -v : v;
+    }
+    const double ad = warp_sum_d((double)acc);
+    if ((threadIdx.x & 31) == 0) atomicAdd(tacc + k, ad);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < n_terms; k += blockDim.x)
+    partials[((size_t)row * n_terms + k) * chunks + chunk] = tacc[k] * (double)coefs[row * cstride + k];
+}
+
+__global__ void pauli_apply_kernel(const float2* __restrict__ psi, float2* __restrict__ lam, int n, int n_terms,
+                                   const uint32_t* xm, const uint32_t* zm, const int32_t* ny, const float* coefs,
+                                   int64_t cstride) {
+  const size_t id = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t dim = (size_t)1 << n;
+  const int row = blockIdx.y;
+  if (id >= dim) return;
+  const uint32_t y = (uint32_t)id;
+  const float2* p = psi + (size_t)row * dim;
+  float2 acc = make_float2(0.f, 0.f);
+  for (int k = 0; k < n_terms; ++k) {
+    const uint32_t x = y ^ xm[k];
+    const float2 a = p[x];
+    float c = coefs[row * cstride + k];
+    if (__popc(x & zm[k]) & 1) c = -c;
+    const int q = ny[k] & 3;  // i^q * a
+    float2 t = q == 0 ? a : q == 1 ? make_float2(-a.y, a.x) : q == 2 ? make_float2(-a.x, -a.y) : make_float2(a.y, -a.x);
+    acc.x = fmaf(c, t.x, acc.x);
+    acc.y = fmaf(c, t.y, acc.y);
+  }
+  lam[(size_t)row * dim + y] = acc;
+}
+
+// ---------------------------------------------------------------------------
+// sampler: numpy Generator(Philox).choice(N, shots, p) semantics
+// ---------------------------------------------------------------------------
+
+constexpr int kChunk = 1024;  // amplitudes per warp chunk (32 lanes x 32)
+
+__device__ __forceinline__ void philox4x64_10(uint64_t c[4], uint64_t k0, uint64_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+    const uint64_t lo0 = 0xD2E7470EE14C6C93ull * c[0], hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c[0]);
+    const uint64_t lo1 = 0xCA5A826395121157ull * c[2], hi1 = __umul64hi(0xCA5A826395121157ull, c[2]);
+    const uint64_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0;
+    c[1] = lo1;
+    c[2] = n2;
+    c[3] = lo0;
+  }
+}
+
+// uniform number s of a fresh numpy Philox stream with key (k0, k1): block s/4 + 1, word s%4
+__device__ __forceinline__ double philox_uniform(uint64_t k0, uint64_t k1, uint64_t s) {
+  uint64_t c[4] = {s / 4 + 1, 0, 0, 0};
+  philox4x64_10(c, k0, k1);
+  const uint64_t w = c[s & 3];
+  return (double)(w >> 11) * (1.0 / 9007199254740992.0);
+}
+
+__device__ __forceinline__ double lane_chunk_sum(const float2* p) {
+  double s = 0.0;
+#pragma unroll 8
+  for (int j = 0; j < 32; ++j) {
+    const float2 a = p[j];
+    s += (double)a.x * a.x + (double)a.y * a.y;
+  }
+  return s;
+}
+
+__device__ __forceinline__ double warp_incl_scan(double v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  return v;
+}
+
+__global__ void chunk_sum_kernel(const float2* __restrict__ psi, int n, int rows, double* chunk_tot) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nchunk = ((int64_t)1 << n) / kChunk;
+  if (warp >= rows * nchunk) return;
+  const int64_t row = warp / nchunk, c = warp % nchunk;
+  const float2* p = psi + (row << n) + c * kChunk + lane * 32;
+  const double incl = warp_incl_scan(lane_chunk_sum(p), lane);
+  if (lane == 31) chunk_tot[warp] = incl;
+}
+
+__global__ void row_scan_kernel(const double* chunk_tot, int64_t nchunk, double* prefix) {
+  // prefix[row, 0..nchunk] exclusive scan, deterministic (fixed segmentation)
+  __shared__ double seg[1024];
+  const int row = blockIdx.x, t = threadIdx.x, T = blockDim.x;
+  const double* c = chunk_tot + row * nchunk;
+  double* out = prefix + row * (nchunk + 1);
+  const int64_t per = (nchunk + T - 1) / T;
+  const int64_t b = t * per, e = min(nchunk, b + per);
+  double s = 0.0;
+  for (int64_t i = b; i < e; ++i) s += c[i];
+  seg[t] = s;
+  __syncthreads();
+  if (t == 0) {
+    double run = 0.0;
+    for (int i = 0; i < T; ++i) {
+      const double x = seg[i];
+      seg[i] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  double run = seg[t];
+  for (int64_t i = b; i < e; ++i) {
+    out[i] = run;
+    run += c[i];
+  }
+  if (e == nchunk && b < e) out[nchunk] = run;
+  if (nchunk == 0 && t == 0) out[0] = 0.0;
+}
+
+__global__ void draw_kernel(const float2* __restrict__ psi, int n, int rows, int shots, const uint64_t* keys,
+                            const double* prefix, int64_t* out, int32_t* near) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= (int64_t)rows * shots) return;
+  const int row = (int)(warp / shots);
+  const int64_t s = warp % shots;
+  const int64_t nchunk = ((int64_t)1 << n) / kChunk;
+  const double* pre = prefix + row * (nchunk + 1);
+  const double total = pre[nchunk];
+  const double u = philox_uniform(keys[2 * row], keys[2 * row + 1], (uint64_t)s);
+  const double target = u * total;
+  // largest chunk c with pre[c] <= target  (c < nchunk)
+  int64_t lo = 0, hi = nchunk - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= target) lo = mid;
+    else hi = mid - 1;
+  }
+  const int64_t c = lo;
+  const float2* p = psi + ((int64_t)row << n) + c * kChunk;
+  const double ls = lane_chunk_sum(p + lane * 32);
+  const double incl = warp_incl_scan(ls, lane);
+  const double base = pre[c];
+  const unsigned ball = __ballot_sync(0xffffffffu, base + incl > target);
+  int64_t idx;
+  double before, after;
+  if (ball) {
+    const int L = __ffs(ball) - 1;
+    double acc = base + __shfl_sync(0xffffffffu, incl - ls, L);
+    int j = 31;
+    double prev = acc;
+    const float2* q = p + L * 32;
+    for (int k = 0; k < 32; ++k) {
+      const float2 a = q[k];
+      prev = acc;
+      acc += (double)a.x * a.x + (double)a.y * a.y;
+      if (acc > target) { j = k; break; }
+    }
+    idx = c * kChunk + L * 32 + j;
+    before = prev;
+    after = acc;
+  } else {  // rounding at the chunk edge: clamp to the chunk's last index
+    idx = c * kChunk + kChunk - 1;
+    before = after = base + __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) {
+    out[(int64_t)row * shots + s] = idx;
+    const double tol = 1e-12 * total;
+    if (near && (fabs(after - target) < tol || fabs(target - before) < tol)) atomicAdd(near + row, 1);
+  }
+}
+
+}  // namespace qf
+
+using namespace qf;
+
+// ---------------------------------------------------------------------------
+// extern "C" entry points
+// ---------------------------------------------------------------------------
+
+extern "C" {
+
+const char* qf_last_error(void) { return g_err.c_str(); }
+
+int qf_version(void) { return 1; }
+
+int qf_device_sm_count(int device) {
+  int v = 0;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+  return v;
+}
+
+int qf_build_ops(const QfBuildRecipe* recipe, const float* theta, int64_t theta_stride, int rows, float* mats,
+                 int n_mat, int32_t* angles, int n_ang, void* stream) {
+  if (!recipe || rows < 0) {
+    set_error("qf_build_ops: bad arguments");
+    return 2;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int T = 128;
+  if (recipe->n_dense > 0 && rows > 0) {
+    const int64_t tot = (int64_t)rows * recipe->n_dense;
+    build_dense_kernel<<<(unsigned)((tot + T - 1) / T), T, 0, s>>>(*recipe, theta, theta_stride, rows,
+                                                                   reinterpret_cast<float2*>(mats), n_mat);
+    if (check_launch("build_dense_kernel")) return 1;
+  }
+  if (recipe->n_terms > 0 && rows > 0) {
+    const int64_t tot = (int64_t)rows * recipe->n_terms;
+    build_angle_kernel<<<(unsigned)((tot + T - 1) / T), T, 0, s>>>(*recipe, theta, theta_stride, rows, angles,
+                                                                   n_ang);
+    if (check_launch("build_angle_kernel")) return 1;
+  }
+  return 0;
+}
+
+static int run_passes_common(const QfProgram* prog, int pb, int pe, float* psi, float* lam, int n, int rows,
+                             const float* mats, const int32_t* angles, const float* coefs, double* partials,
+                             int tiles_per_row, bool adj, void* stream) {
+  if (!prog || n < prog->L || n > 32 || rows < 0) {
+    set_error("qf_run_passes: bad arguments (n=%d L=%d)", n, prog ? prog->L : -1);
+    return 2;
+  }
+  if (rows == 0) return 0;
+  if ((1 << (n - prog->L)) != tiles_per_row) {
+    set_error("tiles_per_row %d does not match n=%d L=%d", tiles_per_row, n, prog->L);
+    return 2;
+  }
+  const QfPass* host_passes = prog->host_passes;
+  PassArgs a;
+  a.prog = *prog;
+  a.psi = reinterpret_cast<float2*>(psi);
+  a.lam = reinterpret_cast<float2*>(lam);
+  a.mats = reinterpret_cast<const float2*>(mats);
+  a.angles = angles;
+  a.coefs = coefs;
+  a.partials = partials;
+  a.n = n;
+  a.rows = rows;
+  a.tiles_log2 = n - prog->L;
+  for (int p = pb; p < pe; ++p) {
+    a.pass = p;
+    int rc = run_pass(a, host_passes[p], adj, (cudaStream_t)stream);
+    if (rc) return rc;
+    if (check_launch(adj ? "adjoint pass" : "forward pass")) return 1;
+  }
+  return 0;
+}
+
+int qf_run_passes(const QfProgram* prog, int pass_begin, int pass_end, float* psi, int n, int rows,
+                  const float* mats, const int32_t* angles, const float* coefs, double* partials, int tiles_per_row,
+                  void* stream) {
+  return run_passes_common(prog, pass_begin, pass_end, psi, nullptr, n, rows, mats, angles, coefs, partials,
+                           tiles_per_row, false, stream);
+}
+
+int qf_adjoint_passes(const QfProgram* prog, int pass_begin, int pass_end, float* psi, float* lam, int n, int rows,
+                      const float* mats, const int32_t* angles, const float* coefs, double* partials,
+                      int tiles_per_row, void* stream) {
+  return run_passes_common(prog, pass_begin, pass_end, psi, lam, n, rows, mats, angles, coefs, partials,
+                           tiles_per_row, true, stream);
+}
+
+int qf_reduce_slots(const double* partials, int rows, int n_slots, int tiles, const int32_t* col_ptr,
+                    const int32_t* slot_list, int n_cols, double* out, int accumulate, void* stream) {
+  if (rows == 0 || n_cols == 0) return 0;
+  const int64_t warps = (int64_t)rows * n_cols;
+  const int T = 256;
+  reduce_slots_kernel<<<(unsigned)((warps * 32 + T - 1) / T), T, 0, (cudaStream_t)stream>>>(
+      partials, rows, n_slots, tiles, col_ptr, slot_list, n_cols, out, accumulate);
+  return check_launch("reduce_slots_kernel");
+}
+
+int qf_pauli_expect(const float* psi, int n, int rows, int n_terms, const uint32_t* xmask, const uint32_t* zmask,
+                    const int32_t* ny, const float* coefs, int64_t coef_stride, double* partials, void* stream) {
+  if (rows == 0 || n_terms == 0) return 0;
+  if (n > 32) {
+    set_error("qf_pauli_expect: n=%d > 32", n);
+    return 2;
+  }
+  const int chunks = (int)(((int64_t)1 << n) + kExpectChunk - 1) / kExpectChunk;
+  dim3 grid(chunks, rows);
+  pauli_expect_kernel<<<grid, 256, n_terms * sizeof(double), (cudaStream_t)stream>>>(
+      reinterpret_cast<const float2*>(psi), n, n_terms, xmask, zmask, ny, coefs, coef_stride, partials, chunks);
+  return check_launch("pauli_expect_kernel");
+}
+
+int qf_pauli_apply(const float* psi, float* lam, int n, int rows, int n_terms, const uint32_t* xmask,
+                   const uint32_t* zmask, const int32_t* ny, const float* coefs, int64_t coef_stride, void* stream) {
+  if (rows == 0) return 0;
+  const int64_t dim = (int64_t)1 << n;
+  dim3 grid((unsigned)((dim + 255) / 256), rows);
+  pauli_apply_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float2*>(psi),
+                                                              reinterpret_cast<float2*>(lam), n, n_terms, xmask,
+                                                              zmask, ny, coefs, coef_stride);
+  return check_launch("pauli_apply_kernel");
+}
+
+int qf_sample(const float* psi, int n, int rows, int shots, const uint64_t* keys, double* scratch, int64_t* out_idx,
+              int32_t* near_boundary, void* stream) {
+  if (rows == 0 || shots == 0) return 0;
+  if (n < 10 || n > 32) {
+    set_error("qf_sample: n=%d outside [10, 32] (callers pad small registers)", n);
+    return 2;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nchunk = ((int64_t)1 << n) / kChunk;
+  double* chunk_tot = scratch;
+  double* prefix = scratch + rows * nchunk;
+  const float2* p = reinterpret_cast<const float2*>(psi);
+  const int64_t warps = rows * nchunk;
+  chunk_sum_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(p, n, rows, chunk_tot);
+  if (check_launch("chunk_sum_kernel")) return 1;
+  row_scan_kernel<<<rows, 1024, 0, s>>>(chunk_tot, nchunk, prefix);
+  if (check_launch("row_scan_kernel")) return 1;
+  const int64_t dw = (int64_t)rows * shots;
+  draw_kernel<<<(unsigned)((dw * 32 + 255) / 256), 256, 0, s>>>(p, n, rows, shots, keys, prefix, out_idx,
+                                                               near_boundary);
+  return check_launch("draw_kernel");
+}
+
+}  // extern "C"

@@ -1,0 +1,417 @@
+"""Batched execution engine: plan cache, device programs, and the call sequence
+(build ops -> forward passes -> expectations -> adjoint passes -> slot reductions).
+
+Everything numeric runs in libqfb200.so kernels on the current CUDA stream; torch
+is used for device allocation and host<->device copies only.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from . import planner as pl
+from .circuit import circuit_symbols
+from .pauli import as_pauli_sum, term_masks
+
+
+def _require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2003_02989_b200 needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+class DeviceProgram:
+    """A planner.Program uploaded to one device + its ctypes descriptor."""
+
+    def __init__(self, prog: pl.Program, device: torch.device):
+        self.prog = prog
+        self.device = device
+
+        def up(a, dtype):
+            a = np.ascontiguousarray(a)
+            if a.size == 0:
+                a = np.zeros(1, dtype=a.dtype)
+            return torch.from_numpy(a).to(device=device, dtype=dtype)
+
+        self.t_passes = up(prog.passes, torch.int32)
+        self.t_stages = up(prog.stages, torch.int32)
+        self.t_ops = up(prog.ops, torch.int32)
+        self.t_mask = up(prog.term_mask.view(np.int32), torch.int32)
+        self.t_idx = up(prog.term_idx, torch.int32)
+        self.t_w = up(prog.term_w, torch.float32)
+        self.t_grp = up(prog.grp, torch.int32)
+        self.t_gen = up(prog.genmats, torch.float32)
+        self.h_passes = np.ascontiguousarray(prog.passes)
+        self.struct = nat.QfProgram(
+            passes=_ptr(self.t_passes), stages=_ptr(self.t_stages), ops=_ptr(self.t_ops),
+            term_mask=_ptr(self.t_mask), term_idx=_ptr(self.t_idx), term_w=_ptr(self.t_w),
+            grp=_ptr(self.t_grp), genmats=_ptr(self.t_gen),
+            n_passes=len(prog.passes), n_slots=prog.n_slots, n_mat=prog.n_mat, n_ang=prog.n_ang,
+            n_coef=prog.n_coef, L=prog.L, R=prog.R, coef_row_stride=0,
+            host_passes=self.h_passes.ctypes.data,
+        )
+        r = prog.recipe
+        self.r_arrays = {k: up(v, _TORCH_OF[np.asarray(v).dtype]) for k, v in r.items()
+                         if isinstance(v, np.ndarray)}
+        self.n_gen = len(r["gen_sym"])
+        self.n_fixed = r["n_fixed"]
+        self.n_const = r["n_const"]
+        self.n_dense = len(r["dense_mat"])
+        self.n_terms = len(r["term_beta"])
+        self.tiles = 1 << (prog.n - prog.L)
+
+    def recipe(self, fixed_t, fixed_rows, const_t, const_rows) -> nat.QfBuildRecipe:
+        a = self.r_arrays
+        return nat.QfBuildRecipe(
+            n_gen=self.n_gen, gen_sym=_ptr(a["gen_sym"]), gen_coeff=_ptr(a["gen_coeff"]),
+            gen_const=_ptr(a["gen_const"]), gen_dim=_ptr(a["gen_dim"]), gen_eval=_ptr(a["gen_eval"]),
+            gen_evec=_ptr(a["gen_evec"]), n_fixed=max(self.n_fixed, 1), fixed=_ptr(fixed_t),
+            fixed_rows=fixed_rows, n_dense=self.n_dense, dense_mat=_ptr(a["dense_mat"]),
+            dense_dim=_ptr(a["dense_dim"]), dense_fbeg=_ptr(a["dense_fbeg"]), factor=_ptr(a["factor"]),
+            n_terms=self.n_terms, term_src=_ptr(a["term_src"]), term_beta=_ptr(a["term_beta"]),
+            term_const=_ptr(const_t), const_rows=const_rows, n_const=max(self.n_const, 1),
+        )
+
+    def csr(self, mapping: dict, n_cols: int):
+        ptr = [0]
+        lst = []
+        for c in range(n_cols):
+            lst.extend(mapping.get(c, []))
+            ptr.append(len(lst))
+        return (torch.tensor(ptr, dtype=torch.int32, device=self.device),
+                torch.tensor(lst or [0], dtype=torch.int32, device=self.device))
+
+
+_TORCH_OF = {
+    np.dtype(np.int32): torch.int32, np.dtype(np.float64): torch.float64,
+    np.dtype(np.float32): torch.float32, np.dtype(np.int64): torch.int64,
+}
+
+
+@dataclass
+class ObsInfo:
+    """Observables split into exact identity constants, fused diagonal ones and generic ones."""
+    sums: list
+    ident: np.ndarray                 # [n_obs] identity coefficient
+    diag_ids: list
+    generic_ids: list
+    key: tuple = ()
+
+
+def analyse_observables(observables) -> ObsInfo:
+    sums = [as_pauli_sum(o) for o in observables]
+    ident = np.zeros(len(sums))
+    stripped = []
+    diag_ids, generic_ids = [], []
+    for k, s in enumerate(sums):
+        terms = []
+        for t in s.terms:
+            if not t.factors:
+                ident[k] += t.coefficient
+            else:
+                terms.append(t)
+        stripped.append(terms)
+        if terms and all(term_masks(t)[0] == 0 for t in terms):
+            diag_ids.append(k)
+        elif terms:
+            generic_ids.append(k)
+    key = tuple(tuple(tuple(sorted(t.factors.items())) for t in stripped[k]) for k in diag_ids)
+    return ObsInfo(stripped, ident, diag_ids, generic_ids, key)
+
+
+@dataclass
+class Plan:
+    n: int
+    n_eff: int
+    S: int
+    infos: list
+    fwd: DeviceProgram
+    adj: DeviceProgram | None = None
+    lam_diag: bool = False
+    obs: ObsInfo | None = None
+    extra: dict = field(default_factory=dict)
+
+
+class Bound:
+    """Everything of a batched call that does not depend on the symbol values:
+    plan, concrete-gate tables, observable coefficient tables and reduction maps,
+    all resident on the device.  ``execute`` then only launches kernels."""
+
+    def __init__(self, engine, circuits, symbol_names, observables, want_grad, device):
+        self.device = device
+        self.symbol_names = list(symbol_names)
+        sym_index = {s: i for i, s in enumerate(self.symbol_names)}
+        self.circuits = list(circuits)
+        template = self.circuits[0]
+        for c in self.circuits:
+            if c.num_qubits != template.num_qubits:
+                raise ValueError("all circuits of a batch must have the same register size")
+            for s in circuit_symbols(c):
+                if s not in sym_index:
+                    raise KeyError(f"missing binding for symbol '{s}'")
+        n = template.num_qubits
+        if n > 32:
+            raise MemoryError(f"{n} qubits exceeds the engine limit of 32 per device")
+        self.obs = obs = analyse_observables(observables)
+        self.n_obs = len(obs.sums)
+        self.S = len(self.symbol_names)
+        self.want_grad = want_grad
+        # weighted Hamiltonian structure for the adjoint: H_b = sum_k up[b,k] obs_k
+        self.lam_diag = False
+        self.hkeys = []
+        if want_grad:
+            uniq: dict = {}
+            for k, terms in enumerate(obs.sums):
+                for t in terms:
+                    uniq.setdefault(tuple(sorted(t.factors.items())), []).append((k, t.coefficient))
+            self.hkeys = list(uniq)
+            M = np.zeros((max(self.n_obs, 1), max(len(self.hkeys), 1)))
+            for j, kk in enumerate(self.hkeys):
+                for k, c in uniq[kk]:
+                    M[k, j] += c
+            self.hmix = torch.from_numpy(M).to(device)
+            self.lam_diag = bool(self.hkeys) and all(all(p == "Z" for _, p in kk) for kk in self.hkeys)
+        self.plan = engine.plan(template, sym_index, obs, want_grad, self.lam_diag,
+                                tuple(self.hkeys) if want_grad else None, device)
+        plan = self.plan
+        fixed_np, const_np = pl.concrete_tables(self.circuits, plan.infos)
+        self.fixed_rows, self.const_rows = fixed_np.shape[0], const_np.shape[0]
+        self.fixed_t = torch.from_numpy(fixed_np.view(np.float64)).to(device)
+        self.const_t = torch.from_numpy(const_np).to(device)
+        if plan.adj is not None:
+            infos_a = plan.extra["adj_infos"]
+            fa, ca = pl.concrete_tables(self.circuits, infos_a)
+            self.fixed_a = torch.from_numpy(fa.view(np.float64)).to(device)
+            self.const_a = torch.from_numpy(ca).to(device)
+            self.fixed_a_rows, self.const_a_rows = fa.shape[0], ca.shape[0]
+        fw = plan.fwd
+        coef_np = np.zeros(max(fw.prog.n_coef, 1), dtype=np.float32)
+        col = 0
+        for k in obs.diag_ids:
+            for t in obs.sums[k]:
+                coef_np[col] = t.coefficient
+                col += 1
+        self.fwd_coefs = torch.from_numpy(coef_np).to(device)
+        self.obs_csr = fw.csr(fw.prog.obs_slots, self.n_obs)
+        self.ident = torch.from_numpy(obs.ident).to(device)
+        # generic (non-diagonal) observables
+        self.gen_T = 0
+        if obs.generic_ids:
+            xs, zs, ys, cs, owner = [], [], [], [], []
+            for k in obs.generic_ids:
+                for t in obs.sums[k]:
+                    xm, zm, ny = term_masks(t)
+                    xs.append(xm); zs.append(zm); ys.append(ny); cs.append(t.coefficient); owner.append(k)
+            self.gen_T = len(xs)
+            self.gen_arrays = (torch.tensor(np.array(xs, dtype=np.uint32).view(np.int32), device=device),
+                               torch.tensor(np.array(zs, dtype=np.uint32).view(np.int32), device=device),
+                               torch.tensor(ys, dtype=torch.int32, device=device),
+                               torch.tensor(cs, dtype=torch.float32, device=device))
+            mapping: dict = {}
+            for j, k in enumerate(owner):
+                mapping.setdefault(k, []).append(j)
+            self.gen_csr = fw.csr(mapping, self.n_obs)
+        if want_grad:
+            ad = plan.adj
+            self.grad_csr = ad.csr(ad.prog.grad_slots, self.S)
+            self.energy_csr = ad.csr({0: ad.prog.energy_slots}, 1)
+            if not self.lam_diag and self.hkeys:
+                xs, zs, ys = [], [], []
+                for kk in self.hkeys:
+                    xm, zm, ny = term_masks(_Term(dict(kk), 1.0))
+                    xs.append(xm); zs.append(zm); ys.append(ny)
+                self.h_arrays = (torch.tensor(np.array(xs, dtype=np.uint32).view(np.int32), device=device),
+                                 torch.tensor(np.array(zs, dtype=np.uint32).view(np.int32), device=device),
+                                 torch.tensor(ys, dtype=torch.int32, device=device))
+
+    @property
+    def B(self):
+        return len(self.circuits)
+
+    def execute(self, theta: torch.Tensor, *, upstream=None, want_state=False, want_grad=False,
+                want_expect=True, stream=None) -> dict:
+        """theta: device float32 [B, S].  Returns device tensors."""
+        lib = nat.load()
+        dev = self.device
+        plan = self.plan
+        B = self.B
+        if stream is None:
+            stream = torch.cuda.current_stream(dev).cuda_stream
+        if theta.shape[1] == 0:
+            theta = torch.zeros((B, 1), dtype=torch.float32, device=dev)
+        fw = plan.fwd
+        n_eff = plan.n_eff
+        psi = torch.empty((B, 1 << n_eff), dtype=torch.complex64, device=dev)
+        mats = torch.empty((B, max(fw.prog.n_mat, 1)), dtype=torch.complex64, device=dev)
+        angs = torch.empty((B, max(fw.prog.n_ang, 1)), dtype=torch.int32, device=dev)
+        rec = fw.recipe(self.fixed_t, self.fixed_rows, self.const_t, self.const_rows)
+        nat.check(lib.qf_build_ops(C.byref(rec), _ptr(theta), theta.shape[1], B, _ptr(mats), fw.prog.n_mat,
+                                   _ptr(angs), fw.prog.n_ang, stream))
+        partials = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
+        nat.check(lib.qf_run_passes(C.byref(fw.struct), 0, len(fw.prog.passes), _ptr(psi), n_eff, B, _ptr(mats),
+                                    _ptr(angs), _ptr(self.fwd_coefs), _ptr(partials), fw.tiles, stream))
+        out: dict = {}
+        if self.n_obs and want_expect:
+            expv = torch.zeros((B, self.n_obs), dtype=torch.float64, device=dev)
+            if self.obs.diag_ids:
+                ptr, lst = self.obs_csr
+                nat.check(lib.qf_reduce_slots(_ptr(partials), B, fw.prog.n_slots, fw.tiles, _ptr(ptr), _ptr(lst),
+                                              self.n_obs, _ptr(expv), 0, stream))
+            if self.gen_T:
+                xm, zm, ny, cf = self.gen_arrays
+                chunks = ((1 << n_eff) + 2047) // 2048
+                part = torch.empty((B, self.gen_T, chunks), dtype=torch.float64, device=dev)
+                nat.check(lib.qf_pauli_expect(_ptr(psi), n_eff, B, self.gen_T, _ptr(xm), _ptr(zm), _ptr(ny),
+                                              _ptr(cf), 0, _ptr(part), stream))
+                ptr, lst = self.gen_csr
+                nat.check(lib.qf_reduce_slots(_ptr(part), B, self.gen_T, chunks, _ptr(ptr), _ptr(lst), self.n_obs,
+                                              _ptr(expv), 1, stream))
+            expv += self.ident
+            out["expectations"] = expv
+        if want_state:
+            st = psi[:, : (1 << plan.n)]
+            out["state"] = st.clone() if want_grad else st
+        if want_grad:
+            self._adjoint(lib, psi, theta, upstream, stream, out)
+        return out
+
+    def _adjoint(self, lib, psi, theta, upstream, stream, out):
+        plan, dev, B = self.plan, self.device, self.B
+        ad = plan.adj
+        n_eff = plan.n_eff
+        if upstream is None:
+            up = torch.ones((B, max(self.n_obs, 1)), dtype=torch.float64, device=dev)
+        else:
+            up = torch.as_tensor(upstream, dtype=torch.float64).to(dev).reshape(B, -1)
+            if up.shape[1] != self.n_obs:
+                raise ValueError(f"upstream shape {tuple(up.shape)} != ({B}, {self.n_obs})")
+        hw_t = (up @ self.hmix).to(torch.float32).contiguous()
+        mats = torch.empty((B, max(ad.prog.n_mat, 1)), dtype=torch.complex64, device=dev)
+        angs = torch.empty((B, max(ad.prog.n_ang, 1)), dtype=torch.int32, device=dev)
+        rec = ad.recipe(self.fixed_a, self.fixed_a_rows, self.const_a, self.const_a_rows)
+        nat.check(lib.qf_build_ops(C.byref(rec), _ptr(theta), theta.shape[1], B, _ptr(mats), ad.prog.n_mat,
+                                   _ptr(angs), ad.prog.n_ang, stream))
+        lam = torch.empty_like(psi)
+        if not self.lam_diag:
+            if self.hkeys:
+                xm, zm, ny = self.h_arrays
+                nat.check(lib.qf_pauli_apply(_ptr(psi), _ptr(lam), n_eff, B, len(self.hkeys), _ptr(xm), _ptr(zm),
+                                             _ptr(ny), _ptr(hw_t), hw_t.shape[1], stream))
+            else:
+                lam.zero_()
+        struct = nat.QfProgram.from_buffer_copy(ad.struct)
+        struct.coef_row_stride = hw_t.shape[1]
+        partials = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
+        nat.check(lib.qf_adjoint_passes(C.byref(struct), 0, len(ad.prog.passes), _ptr(psi), _ptr(lam), n_eff, B,
+                                        _ptr(mats), _ptr(angs), _ptr(hw_t), _ptr(partials), ad.tiles, stream))
+        grad = torch.zeros((B, max(self.S, 1)), dtype=torch.float64, device=dev)
+        if self.S:
+            ptr, lst = self.grad_csr
+            nat.check(lib.qf_reduce_slots(_ptr(partials), B, ad.prog.n_slots, ad.tiles, _ptr(ptr), _ptr(lst), self.S,
+                                          _ptr(grad), 0, stream))
+        if self.lam_diag:
+            energy = torch.empty((B, 1), dtype=torch.float64, device=dev)
+            ptr, lst = self.energy_csr
+            nat.check(lib.qf_reduce_slots(_ptr(partials), B, ad.prog.n_slots, ad.tiles, _ptr(ptr), _ptr(lst), 1,
+                                          _ptr(energy), 0, stream))
+            out["energy"] = energy[:, 0]
+        out["grad"] = grad[:, : self.S]
+
+
+class Engine:
+    def __init__(self, max_bound: int = 64):
+        self._plans: dict = {}
+        self._bound: dict = {}
+        self._max_bound = max_bound
+        self._lock = threading.Lock()
+
+    def plan(self, template, symbol_index, obs: ObsInfo, adjoint: bool, lam_diag: bool, hkeys, device):
+        topo = pl.topology_key(template, symbol_index)
+        key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device))
+        with self._lock:
+            hit = self._plans.get(key)
+        if hit is not None:
+            return hit
+        n = template.num_qubits
+        n_eff = max(n, pl.N_MIN)
+        infos = pl.analyse(template, symbol_index)
+        diag_sums = [None] * len(obs.sums)
+        for k in obs.diag_ids:
+            diag_sums[k] = _TermList(obs.sums[k])
+        fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
+                               obs_diag_ids=obs.diag_ids)
+        plan = Plan(n, n_eff, len(symbol_index), infos, DeviceProgram(fwd, device), None, lam_diag, obs)
+        if adjoint:
+            infos_a = pl.analyse(template, symbol_index)
+            hterms = _TermList([_Term(dict(kk), 1.0) for kk in hkeys])
+            adjp = pl.build_program(template, infos_a, n_eff, adjoint=True, observables=[hterms],
+                                    lam_diag=lam_diag)
+            plan.adj = DeviceProgram(adjp, device)
+            plan.extra["adj_infos"] = infos_a
+        with self._lock:
+            self._plans[key] = plan
+        return plan
+
+    def bind(self, circuits, symbol_names, observables=(), *, want_grad=False, device=None) -> Bound:
+        dev = _require_cuda(device)
+        symbol_names = tuple(s.name if hasattr(s, "name") else s for s in symbol_names)
+        observables = list(observables)
+        key = (tuple(map(id, circuits)), symbol_names, tuple(map(id, observables)), bool(want_grad), str(dev))
+        with self._lock:
+            hit = self._bound.get(key)
+        if hit is not None and all(a is b for a, b in zip(hit.circuits, circuits)):
+            return hit
+        b = Bound(self, circuits, symbol_names, observables, want_grad, dev)
+        b._keepalive = observables
+        with self._lock:
+            if len(self._bound) >= self._max_bound:
+                self._bound.pop(next(iter(self._bound)))
+            self._bound[key] = b
+        return b
+
+    def run(self, circuits, symbol_names, values, observables=(), *, want_state=False, want_grad=False,
+            upstream=None, device=None):
+        """One-shot convenience: bind (cached) + execute.  values: [B, S]."""
+        dev = _require_cuda(device)
+        vals = values if isinstance(values, torch.Tensor) else torch.as_tensor(np.asarray(values, dtype=np.float32))
+        if vals.ndim == 1:
+            vals = vals.reshape(1, -1) if len(symbol_names) else vals.reshape(-1, 0)
+        B = int(vals.shape[0])
+        if not isinstance(circuits, (list, tuple)):
+            circuits = [circuits] * B
+        if len(circuits) != B:
+            raise ValueError(f"{len(circuits)} circuits for {B} parameter rows")
+        if B == 0:
+            return {}
+        bound = self.bind(circuits, symbol_names, observables, want_grad=want_grad, device=dev)
+        theta = vals.to(device=dev, dtype=torch.float32).contiguous()
+        out = bound.execute(theta, upstream=upstream, want_state=want_state, want_grad=want_grad)
+        out["plan"] = bound.plan
+        return out
+
+
+class _Term:
+    __slots__ = ("factors", "coefficient")
+
+    def __init__(self, factors, coefficient):
+        self.factors = dict(factors)
+        self.coefficient = coefficient
+
+
+class _TermList:
+    def __init__(self, terms):
+        self.terms = list(terms.terms if hasattr(terms, "terms") else terms)
+
+
+ENGINE = Engine()

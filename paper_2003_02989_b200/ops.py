@@ -1,0 +1,193 @@
+"""TFQ-style batched ops on the B200 engine (the north-star call signatures).
+
+``op(circuits[B], symbol_names[S], symbol_values[B, S], operators[n_obs])``
+
+* ``circuits``: one circuit (broadcast over rows) or a list of B circuits sharing
+  a topology (values of concrete gates may differ per row, e.g. data encodings);
+* ``symbol_names``: column order of ``symbol_values``;
+* ``symbol_values``: numpy / CPU tensor (results come back as numpy, float64) or a
+  CUDA tensor (results stay on the device as torch tensors);
+* ``operators``: Pauli sums (this package's or the reference's objects).
+
+Reference semantics: qcflow/sim.py ``batch_execute`` (:275-294) for expectations,
+``sample`` (:223-227) / ``sampled_expectation`` (:245-272) for the shot-based ops,
+and the gradient of ``quantum_backward`` (graph.py:471-513) for the adjoint.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import gates as lib_gates
+from .circuit import Circuit
+from .engine import ENGINE
+from .pauli import as_pauli_sum
+from .sampling import bits_from_indices, derive_seed, philox_key, sample_indices
+
+
+def _prep(circuits, symbol_values, symbol_names):
+    on_dev = isinstance(symbol_values, torch.Tensor) and symbol_values.is_cuda
+    if isinstance(symbol_values, torch.Tensor):
+        vals = symbol_values
+    else:
+        vals = torch.as_tensor(np.asarray(symbol_values, dtype=np.float32))
+    if vals.ndim == 1:
+        vals = vals.reshape(1, -1) if len(symbol_names) else vals.reshape(-1, 0)
+    B = int(vals.shape[0])
+    if not isinstance(circuits, (list, tuple)):
+        circuits = [circuits] * B
+    if len(circuits) != B:
+        raise ValueError(f"{len(circuits)} circuits for {B} parameter rows")
+    if B and vals.shape[1] != len(symbol_names):
+        raise ValueError(f"symbol_values has {vals.shape[1]} columns for {len(symbol_names)} symbol names")
+    return list(circuits), vals, B, on_dev
+
+
+def _to_dev(vals, dev):
+    if vals.is_cuda:
+        return vals.to(dtype=torch.float32).contiguous()
+    if vals.dtype != torch.float32:
+        vals = vals.to(torch.float32)
+    return vals.to(dev, non_blocking=vals.is_pinned()).contiguous()
+
+
+def _out(t, on_dev):
+    return t if on_dev else t.cpu().numpy()
+
+
+def expectation(circuits, symbol_names, symbol_values, operators):
+    """[B, n_obs] exact expectations (float64)."""
+    circuits, vals, B, on_dev = _prep(circuits, symbol_values, symbol_names)
+    ops = [as_pauli_sum(o) for o in operators]
+    if B == 0:
+        return np.zeros((0, len(ops)))
+    bound = ENGINE.bind(circuits, symbol_names, ops)
+    out = bound.execute(_to_dev(vals, bound.device))
+    return _out(out["expectations"], on_dev)
+
+
+def expectation_and_gradient(circuits, symbol_names, symbol_values, operators, upstream=None):
+    """(expectations [B, n_obs], d<sum_k upstream[b,k] O_k>/d symbol_values [B, S]) via the
+    adjoint method (one forward + one backward sweep per batch)."""
+    circuits, vals, B, on_dev = _prep(circuits, symbol_values, symbol_names)
+    ops = [as_pauli_sum(o) for o in operators]
+    if B == 0:
+        return np.zeros((0, len(ops))), np.zeros((0, len(symbol_names)))
+    bound = ENGINE.bind(circuits, symbol_names, ops, want_grad=True)
+    out = bound.execute(_to_dev(vals, bound.device), upstream=upstream, want_grad=True)
+    return _out(out["expectations"], on_dev), _out(out["grad"], on_dev)
+
+
+def state(circuits, symbol_names, symbol_values):
+    """[B, 2^n] complex64 final states (device tensor; numpy complex64 for host inputs)."""
+    circuits, vals, B, on_dev = _prep(circuits, symbol_values, symbol_names)
+    bound = ENGINE.bind(circuits, symbol_names, [])
+    out = bound.execute(_to_dev(vals, bound.device), want_state=True, want_expect=False)
+    return _out(out["state"], on_dev)
+
+
+def _row_seeds(seed, B):
+    if isinstance(seed, (list, tuple, np.ndarray)):
+        if len(seed) != B:
+            raise ValueError("need one seed per row")
+        return [int(s) for s in seed]
+    return [derive_seed(int(seed), b) for b in range(B)]
+
+
+def sample(circuits, symbol_names, symbol_values, repetitions: int, seed=0):
+    """Bitstrings [B, repetitions, n] uint8 (column q = qubit q); row b draws with
+    substream(seed_b) where seed_b = seed[b] or derive_seed(seed, b) (ref sim.py:223-227)."""
+    if repetitions < 1:
+        raise ValueError("shots must be >= 1")
+    circuits, vals, B, on_dev = _prep(circuits, symbol_values, symbol_names)
+    bound = ENGINE.bind(circuits, symbol_names, [])
+    out = bound.execute(_to_dev(vals, bound.device), want_state=True, want_expect=False)
+    n = bound.plan.n
+    psi = out["state"] if bound.plan.n_eff == n else _padded(out["state"], bound.plan.n_eff)
+    keys = [philox_key(s) for s in _row_seeds(seed, B)]
+    idx, _ = sample_indices(psi, bound.plan.n_eff, repetitions, keys)
+    return bits_from_indices(idx.cpu().numpy(), n)
+
+
+def _padded(st, n_eff):
+    B, d = st.shape
+    full = torch.zeros((B, 1 << n_eff), dtype=st.dtype, device=st.device)
+    full[:, :d] = st
+    return full
+
+
+def _basis_gates(term):
+    """ref sim.py:230-242: H for X; Z**-0.5 then H for Y."""
+    out = []
+    for q, p in sorted(term.factors.items()):
+        if p == "X":
+            out.append(lib_gates.h(q))
+        elif p == "Y":
+            out.append(lib_gates.zpow(-0.5, q))
+            out.append(lib_gates.h(q))
+    return out
+
+
+def sampled_expectation(circuits, symbol_names, symbol_values, operators, repetitions: int, seed=0):
+    """[B, n_obs] shot estimates with the reference's per-term semantics: term k of an
+    operator is measured in its own rotated basis with substream(seed_b, k)
+    (ref sim.py:245-272; seed_b as in :func:`sample`).  Terms sharing a basis rotation
+    share one simulated state."""
+    if repetitions < 1:
+        raise ValueError("shots_per_term must be >= 1")
+    circuits, vals, B, on_dev = _prep(circuits, symbol_values, symbol_names)
+    seeds = _row_seeds(seed, B)
+    ops = [as_pauli_sum(o) for o in operators]
+    res = np.zeros((B, len(ops)))
+    # group (op, term) by basis rotation signature
+    groups: dict = {}
+    for oi, o in enumerate(ops):
+        parts = []
+        for k, t in enumerate(o.terms):
+            if not t.factors:
+                parts.append(("ident", t.coefficient))
+                continue
+            sig = tuple(sorted((q, p) for q, p in t.factors.items() if p != "Z"))
+            groups.setdefault(sig, []).append((oi, k, t))
+            parts.append(("term", k))
+        ops[oi] = (o, parts)
+    values_per_term: dict = {}
+    for sig, members in groups.items():
+        extra = _basis_gates(members[0][2].__class__(1.0, dict(sig))) if sig else []
+        rot = [Circuit(c.num_qubits, tuple(c.gates) + tuple(extra)) for c in circuits] if extra else circuits
+        bound = ENGINE.bind(rot, symbol_names, [])
+        st = bound.execute(_to_dev(vals, bound.device), want_state=True, want_expect=False)["state"]
+        n, n_eff = bound.plan.n, bound.plan.n_eff
+        psi = st if n_eff == n else _padded(st, n_eff)
+        for oi, k, t in members:
+            keys = [philox_key(seeds[b], k) for b in range(B)]
+            idx, _ = sample_indices(psi, n_eff, repetitions, keys)
+            idx = idx.cpu().numpy()
+            mask = 0
+            for q in t.factors:
+                mask |= 1 << q
+            par = np.zeros(idx.shape, dtype=np.int64)
+            m = idx & mask
+            while np.any(m):
+                par ^= m & 1
+                m = m >> 1
+            eig = 1.0 - 2.0 * par
+            values_per_term[(oi, k)] = t.coefficient * eig.mean(axis=1)
+    for oi, (o, parts) in enumerate(ops):
+        contrib = []
+        for kind, x in parts:
+            contrib.append(np.full(B, x) if kind == "ident" else values_per_term[(oi, x)])
+        res[:, oi] = _pairwise(contrib) if contrib else 0.0
+    return res
+
+
+def _pairwise(values):
+    """Deterministic pairwise tree (ref sim.py:162-174), applied elementwise over rows."""
+    work = list(values)
+    while len(work) > 1:
+        nxt = [work[i] + work[i + 1] for i in range(0, len(work) - 1, 2)]
+        if len(work) % 2:
+            nxt.append(work[-1])
+        work = nxt
+    return work[0]

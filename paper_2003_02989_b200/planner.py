@@ -1,0 +1,853 @@
+"""Topology planner: circuit -> fused ops -> tile passes -> register stages -> device program.
+
+This replaces the per-row host work of the reference (``resolve`` + ``gate_matrix`` +
+``fuse_resolved`` per row and per evaluation, qcflow/sim.py:116-136,
+fusion.py:78-176) with a plan that is built ONCE per circuit topology and shared
+by every batch row; the per-row numbers (matrices, phase angles) are produced on
+the GPU by ``qf_build_ops`` from the ``[batch, n_symbols]`` value matrix.
+
+Fusion here differs from the reference's qsim-style pass in what it is optimised
+for, not in results: 1q runs are merged, 1q gates fold into neighbouring dense
+2q gates, and every diagonal gate (Z-type generators, CZ, S, T, ...) becomes a
+term of a *phase polynomial* ``exp(-i sum_k theta_k Z_{m_k})`` that the kernel
+evaluates from the amplitude index without moving data.  Adjoint programs keep
+every symbolic gate separate (a gradient slot each) and only fuse fixed gates.
+
+Geometry (see csrc/qf_pass.cu): a pass owns a tile of L qubits that always
+contains qubits 0..4 (coalesced 256-byte warp accesses); inside a pass, stages
+choose which R tile bits live in registers; dense ops must sit on register bits.
+"""
+
+from __future__ import annotations
+
+import heapq
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .circuit import generator_matrix, gate_matrix
+from .pauli import term_masks
+
+N_MIN = 10          # smaller registers are padded (extra qubits stay |0>)
+LANE_Q = 5          # qubits 0..4 are always lane bits at load/store
+FWD_L, FWD_R = 13, 5
+ADJ_L, ADJ_R = 12, 4
+
+OP_DENSE1, OP_DENSE2, OP_DIAG, OP_OBS = 1, 2, 3, 4
+INIT_LOAD, INIT_ZERO, INIT_PRODUCT, INIT_LOAD_PSI = 0, 1, 2, 3
+
+STAGE_INTS, OP_INTS, PASS_INTS = 64, 16, 128
+
+
+def swizzle(l: int) -> int:
+    """GF(2)-linear smem swizzle: low 4 bits ^= bits 4-7 ^ 8-11 ^ 12-15."""
+    return l ^ ((l >> 4) & 15) ^ ((l >> 8) & 15) ^ ((l >> 12) & 15)
+
+
+# ---------------------------------------------------------------------------
+# gate analysis
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class GateInfo:
+    index: int
+    targets: tuple
+    symbolic: bool
+    diag: bool
+    sym: int = -1          # symbol column
+    coeff: float = 0.0
+    const: float = 0.0
+    terms: list = field(default_factory=list)   # [(factors dict, coeff)] generator terms
+    gen: int = -1          # index in the generator table (symbolic gates)
+    fixed: int = -1        # index in the fixed-matrix table (concrete dense gates)
+    const_col: int = -1    # first constant-angle column (concrete diagonal gates)
+
+
+def _is_z_only(terms) -> bool:
+    return all(all(p == "Z" for p in f.values()) for f, _ in terms)
+
+
+def _gate_terms(g):
+    return [(dict(t.factors), float(t.coefficient)) for t in g.generator.terms]
+
+
+def topology_key(circuit, symbol_index) -> tuple:
+    """Structure that must match for rows to share one plan (values may differ)."""
+    out = [circuit.num_qubits]
+    for g in circuit.gates:
+        e = g.exponent
+        if e is not None and e.symbol is not None:
+            gen = tuple(sorted((tuple(sorted(t.factors.items())), t.coefficient) for t in g.generator.terms))
+            out.append(("s", tuple(g.targets), symbol_index[e.symbol], e.coeff, e.const, gen))
+        else:
+            out.append(("c", tuple(g.targets), _concrete_is_diag(g)))
+    return tuple(out)
+
+
+_DIAG_CACHE: dict = {}
+
+
+def _concrete_is_diag(g) -> bool:
+    if g.matrix is None:
+        return _is_z_only(_gate_terms(g))
+    key = id(g)
+    hit = _DIAG_CACHE.get(key)
+    if hit is not None and hit[0] is g:
+        return hit[1]
+    m = np.asarray(g.matrix)
+    d = bool(np.all(m[~np.eye(m.shape[0], dtype=bool)] == 0))
+    _DIAG_CACHE[key] = (g, d)
+    return d
+
+
+def analyse(circuit, symbol_index) -> list[GateInfo]:
+    infos = []
+    for i, g in enumerate(circuit.gates):
+        e = g.exponent
+        tg = tuple(int(q) for q in g.targets)
+        if e is not None and e.symbol is not None:
+            terms = _gate_terms(g)
+            infos.append(GateInfo(i, tg, True, _is_z_only(terms), symbol_index[e.symbol],
+                                  float(e.coeff), float(e.const), terms))
+        else:
+            infos.append(GateInfo(i, tg, False, _concrete_is_diag(g)))
+    return infos
+
+
+# ---------------------------------------------------------------------------
+# ops (fusion)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Op:
+    kind: int
+    qubits: tuple                      # DENSE: ordered (msb, lsb) / (q,); DIAG: support
+    factors: list = field(default_factory=list)   # gate indices in application order (dense)
+    gates: list = field(default_factory=list)     # gate indices (diag)
+    symbolic: bool = False
+    sym: int = -1                      # adjoint: the op's single symbol (-1 = none)
+    index: int = 0
+    obs: int = -1                      # OBS: observable id
+    obs_terms: list = field(default_factory=list)  # OBS: [(zmask, coef column)]
+
+
+def _diag_op_qubits(gates, infos):
+    qs = set()
+    for gi in gates:
+        qs.update(infos[gi].targets)
+    return tuple(sorted(qs))
+
+
+def build_ops(infos: list[GateInfo], adjoint: bool) -> list[Op]:
+    """Fuse gates into dense 1q/2q ops and diagonal phase-polynomial ops.
+
+    ``adjoint``: symbolic gates are never merged with anything except that
+    symbolic diagonal gates sharing one symbol share a DIAG op.
+    """
+    ops: list[Op | None] = []
+    last: dict[int, int] = {}   # qubit -> index of last op touching it
+
+    def live(i):
+        return ops[i] is not None
+
+    for gi, info in enumerate(infos):
+        tq = info.targets
+        if info.diag:
+            # walk back over ops that commute with this gate (disjoint or diagonal)
+            # and join the most recent compatible DIAG op
+            target = None
+            for j in range(len(ops) - 1, -1, -1):
+                op = ops[j]
+                if op is None:
+                    continue
+                if op.kind == OP_DIAG:
+                    ok = (not adjoint) or not (info.symbolic and op.symbolic and op.sym != info.sym)
+                    if ok:
+                        target = j
+                        break
+                    continue
+                if set(op.qubits) & set(tq):
+                    break
+            if target is not None:
+                op = ops[target]
+                op.gates.append(gi)
+                op.qubits = _diag_op_qubits(op.gates, infos)
+                if info.symbolic:
+                    op.symbolic = True
+                    op.sym = info.sym
+                for q in tq:
+                    if last.get(q, -1) < target:
+                        last[q] = target
+            else:
+                ops.append(Op(OP_DIAG, tuple(sorted(tq)), gates=[gi], symbolic=info.symbolic,
+                              sym=info.sym if info.symbolic else -1))
+                for q in tq:
+                    last[q] = len(ops) - 1
+            continue
+
+        can_merge_sym = not adjoint
+        if len(tq) == 1:
+            q = tq[0]
+            j = last.get(q)
+            if j is not None and ops[j] is not None and ops[j].kind in (OP_DENSE1, OP_DENSE2):
+                prev = ops[j]
+                if can_merge_sym or (not info.symbolic and not prev.symbolic):
+                    # all later ops touching q: none (j is last on q) -> merge is exact
+                    prev.factors.append(gi)
+                    prev.symbolic |= info.symbolic
+                    continue
+            ops.append(Op(OP_DENSE1, tq, factors=[gi], symbolic=info.symbolic,
+                          sym=info.sym if info.symbolic else -1))
+            last[q] = len(ops) - 1
+            continue
+
+        a, b = tq
+        ja, jb = last.get(a), last.get(b)
+        if ja is not None and ja == jb and ops[ja].kind == OP_DENSE2 and set(ops[ja].qubits) == {a, b} \
+                and (can_merge_sym or (not info.symbolic and not ops[ja].symbolic)):
+            ops[ja].factors.append(gi)
+            ops[ja].symbolic |= info.symbolic
+            continue
+        new = Op(OP_DENSE2, (a, b), factors=[], symbolic=info.symbolic,
+                 sym=info.sym if info.symbolic else -1)
+        # absorb trailing 1q dense ops on a / b (they are the last op on their qubit)
+        for q in (a, b):
+            j = last.get(q)
+            if j is not None and ops[j] is not None and ops[j].kind == OP_DENSE1 and \
+                    (can_merge_sym or (not info.symbolic and not ops[j].symbolic)):
+                new.factors.extend(ops[j].factors)
+                new.symbolic |= ops[j].symbolic
+                ops[j] = None
+        new.factors.append(gi)
+        ops.append(new)
+        last[a] = last[b] = len(ops) - 1
+
+    out = [o for o in ops if o is not None]
+    for i, o in enumerate(out):
+        o.index = i
+    return out
+
+
+def dependencies(ops: list[Op]) -> list[set]:
+    """preds[j]: ops that must run before j (diagonal ops commute with each other)."""
+    last_nd: dict[int, int] = {}
+    diag_since: dict[int, list] = {}
+    preds = []
+    for j, op in enumerate(ops):
+        p = set()
+        is_diag = op.kind in (OP_DIAG, OP_OBS)
+        for q in op.qubits:
+            if q in last_nd:
+                p.add(last_nd[q])
+            if not is_diag:
+                p.update(diag_since.get(q, []))
+        preds.append(p)
+        for q in op.qubits:
+            if is_diag:
+                diag_since.setdefault(q, []).append(j)
+            else:
+                last_nd[q] = j
+                diag_since[q] = []
+    return preds
+
+
+def absorb_product_init(ops: list[Op], infos, n: int, allow_symbolic: bool):
+    """Leading 1q dense ops become the product-state initialisation."""
+    first: dict[int, int] = {}
+    for j, op in enumerate(ops):
+        for q in op.qubits:
+            first.setdefault(q, j)
+    init = {}
+    keep = []
+    for j, op in enumerate(ops):
+        if op.kind == OP_DENSE1 and first.get(op.qubits[0]) == j and (allow_symbolic or not op.symbolic):
+            init[op.qubits[0]] = op
+        else:
+            keep.append(op)
+    for i, o in enumerate(keep):
+        o.index = i
+    return keep, init
+
+
+# ---------------------------------------------------------------------------
+# passes and stages
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Stage:
+    regs: list            # local bits in register slots (slot j -> regs[j])
+    ops: list             # Op objects in execution order
+
+
+@dataclass
+class Pass:
+    qubits: list          # sorted global qubits of the tile (local bit i -> qubits[i])
+    ops: list
+    stages: list = field(default_factory=list)
+    init: int = INIT_LOAD
+    store: int = 1
+
+
+class _Sched:
+    def __init__(self, ops, subset=None):
+        self.ops = ops
+        ids = set(range(len(ops))) if subset is None else set(subset)
+        preds = dependencies(ops)
+        self.npred = {j: len([p for p in preds[j] if p in ids]) for j in ids}
+        self.succ = {j: [] for j in ids}
+        for j in ids:
+            for p in preds[j]:
+                if p in ids:
+                    self.succ[p].append(j)
+        self.ready = [j for j in ids if self.npred[j] == 0]
+        heapq.heapify(self.ready)
+        self.left = len(ids)
+
+    def take(self, j):
+        self.left -= 1
+        for s in self.succ[j]:
+            self.npred[s] -= 1
+            if self.npred[s] == 0:
+                heapq.heappush(self.ready, s)
+
+    def drain(self, fits):
+        """Repeatedly take ready ops accepted by ``fits``; return them in order."""
+        taken = []
+        while True:
+            pick = None
+            for j in sorted(self.ready):
+                if fits(self.ops[j]):
+                    pick = j
+                    break
+            if pick is None:
+                return taken
+            self.ready.remove(pick)
+            heapq.heapify(self.ready)
+            self.take(pick)
+            taken.append(self.ops[pick])
+
+
+def plan_passes(ops: list[Op], n: int, L: int) -> list[Pass]:
+    if n == L:
+        return [Pass(list(range(n)), list(ops))] if ops else [Pass(list(range(n)), [])]
+    sch = _Sched(ops)
+    passes = []
+    while sch.left > 0:
+        Q = set(range(LANE_Q))
+        taken = []
+        while True:
+            taken += sch.drain(lambda o: o.kind in (OP_DIAG, OP_OBS) or set(o.qubits) <= Q)
+            cands = [sch.ops[j] for j in sch.ready]
+            if not cands:
+                break
+            best = min(cands, key=lambda o: (len(set(o.qubits) - Q), o.index))
+            if len(Q | set(best.qubits)) > L:
+                break
+            Q |= set(best.qubits)
+        if not taken:
+            raise AssertionError("pass planner made no progress")
+        for q in range(n):
+            if len(Q) >= L:
+                break
+            Q.add(q)
+        passes.append(Pass(sorted(Q), taken))
+    if not passes:
+        passes.append(Pass(list(range(L)), []))
+    return passes
+
+
+def _stage_regs(need: set, R: int, L: int, allow_lanes: bool, prefer: list) -> list:
+    regs = set(need)
+    for b in prefer + list(range(L - 1, -1, -1)):
+        if len(regs) >= R:
+            break
+        if b in regs or (not allow_lanes and b < LANE_Q):
+            continue
+        regs.add(b)
+    return sorted(regs)
+
+
+def plan_stages(p: Pass, R: int) -> None:
+    L = len(p.qubits)
+    loc = {q: i for i, q in enumerate(p.qubits)}
+    ops = p.ops
+    sch = _Sched(ops)
+    stages: list[Stage] = []
+
+    def local_set(o):
+        return {loc[q] for q in o.qubits}
+
+    while sch.left > 0:
+        first = not stages
+        # choose register bits: greedily cover ready dense ops (in index order)
+        need: set = set()
+        virt = _Sched(ops, subset=[j for j in range(len(ops)) if j in sch.npred and sch.npred.get(j, 0) >= 0])
+        # replay the real state into the virtual scheduler
+        virt.npred = dict(sch.npred)
+        virt.ready = list(sch.ready)
+        heapq.heapify(virt.ready)
+        virt.left = sch.left
+        while True:
+            progressed = False
+            for j in sorted(virt.ready):
+                o = ops[j]
+                if o.kind in (OP_DIAG, OP_OBS):
+                    virt.ready.remove(j); heapq.heapify(virt.ready); virt.take(j)
+                    progressed = True
+                    break
+                ls = local_set(o)
+                if first and min(ls) < LANE_Q:
+                    continue
+                if len(need | ls) <= R:
+                    need |= ls
+                    virt.ready.remove(j); heapq.heapify(virt.ready); virt.take(j)
+                    progressed = True
+                    break
+            if not progressed:
+                break
+        upcoming = []
+        for j in sorted(virt.ready):
+            for b in sorted(local_set(ops[j])):
+                if b not in upcoming:
+                    upcoming.append(b)
+        regs = _stage_regs(need, R, L, allow_lanes=not first, prefer=[b for b in upcoming if b >= LANE_Q])
+        rs = set(regs)
+        taken = sch.drain(lambda o: o.kind in (OP_DIAG, OP_OBS) or local_set(o) <= rs)
+        stages.append(Stage(regs, taken))
+        if not taken and not first:
+            raise AssertionError("stage planner made no progress")
+    if not stages:
+        stages.append(Stage(list(range(L - R, L)), []))
+    # store needs lanes on local bits 0..4
+    if min(stages[-1].regs) < LANE_Q:
+        stages.append(Stage(list(range(L - R, L)), []))
+    p.stages = stages
+
+
+def stage_slots(p: Pass, st: Stage, R: int):
+    """(register local bits, thread local bits [lanes first])."""
+    L = len(p.qubits)
+    rs = set(st.regs)
+    free = [b for b in range(L) if b not in rs]
+    lanes = [b for b in range(LANE_Q) if b not in rs]
+    if len(lanes) < LANE_Q:
+        lanes = free[:LANE_Q]
+    warps = [b for b in free if b not in lanes]
+    return list(st.regs), lanes + warps
+
+
+# ---------------------------------------------------------------------------
+# program emission
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class Program:
+    n: int
+    L: int
+    R: int
+    adjoint: bool
+    passes: np.ndarray            # [P, 128] int32
+    stages: np.ndarray            # [S, 64] int32
+    ops: np.ndarray               # [O, 16] int32
+    term_mask: np.ndarray         # uint32
+    term_idx: np.ndarray          # int32
+    term_w: np.ndarray            # float32
+    grp: np.ndarray               # int32
+    genmats: np.ndarray           # float32 interleaved complex
+    n_slots: int
+    n_mat: int
+    n_ang: int
+    n_coef: int
+    # build recipe
+    recipe: dict
+    # slot -> output mapping
+    grad_slots: dict              # symbol column -> [slots]
+    obs_slots: dict               # observable id -> [slots]
+    energy_slots: list
+    stats: dict
+
+
+def _bit_subset(mask: int, reg_glob: list) -> int:
+    s = 0
+    for j, g in enumerate(reg_glob):
+        if mask >> g & 1:
+            s |= 1 << j
+    return s
+
+
+class Emitter:
+    def __init__(self, n, L, R, infos, adjoint):
+        self.n, self.L, self.R, self.infos, self.adjoint = n, L, R, infos, adjoint
+        self.pass_rows, self.stage_rows, self.op_rows = [], [], []
+        self.term_mask, self.term_idx, self.term_w, self.grp = [], [], [], []
+        self.genmats = []
+        self.n_mat = 0
+        self.n_ang = 0
+        self.n_coef = 0
+        self.n_slots = 0
+        self.dense_recipe = []    # (mat offset, dim, factors[(kind, src, emb)])
+        self.term_src = []        # (kind, src, beta)
+        self.grad_slots: dict = {}
+        self.obs_slots: dict = {}
+        self.energy_slots: list = []
+        self.coef_cols = []       # (obs id, term index within observable)
+
+    # -- per-row matrix slab --------------------------------------------------
+    def dense_mat(self, op: Op, order: tuple) -> int:
+        """Reserve slab space for a dense op whose local basis is ``order`` (msb first)."""
+        d = 1 << len(order)
+        off = self.n_mat
+        self.n_mat += d * d
+        facs = []
+        for gi in op.factors:
+            info = self.infos[gi]
+            kind, src = (0, info.gen) if info.symbolic else (1, info.fixed)
+            if len(order) == 1:
+                emb = 4
+            elif len(info.targets) == 2:
+                emb = 0 if tuple(info.targets) == tuple(order) else 1
+            else:
+                emb = 2 if info.targets[0] == order[0] else 3
+            facs.append((kind, src, emb))
+        self.dense_recipe.append((off, d, facs))
+        return off
+
+    def angle_col(self, kind, src, beta) -> int:
+        self.term_src.append((kind, src, beta))
+        self.n_ang += 1
+        return self.n_ang - 1
+
+    def emit_terms(self, terms, reg_glob):
+        """terms: [(zmask, idx, weight)] -> sorted by register subset; returns (begin, end, grp)."""
+        R = self.R
+        keyed = sorted(((_bit_subset(m, reg_glob), m, i, w) for m, i, w in terms), key=lambda x: x[0])
+        begin = len(self.term_mask)
+        bounds = [begin] * ((1 << R) + 1)
+        for s, m, i, w in keyed:
+            self.term_mask.append(m)
+            self.term_idx.append(i)
+            self.term_w.append(w)
+        pos = begin
+        k = 0
+        for S in range(1 << R):
+            bounds[S] = pos
+            while k < len(keyed) and keyed[k][0] == S:
+                k += 1
+                pos += 1
+        bounds[1 << R] = pos
+        g = len(self.grp)
+        self.grp.extend(bounds)
+        return begin, len(self.term_mask), g
+
+    def diag_terms(self, op: Op):
+        """Phase-polynomial terms of a DIAG op: [(zmask, angle column, grad weight)]."""
+        out = []
+        for gi in op.gates:
+            info = self.infos[gi]
+            if info.symbolic:
+                for f, beta in info.terms:
+                    zm = 0
+                    for q in f:
+                        zm |= 1 << q
+                    col = self.angle_col(0, info.gen, beta)
+                    w = 2.0 * info.coeff * beta if (self.adjoint and zm) else 0.0
+                    out.append((zm, col, w))
+            else:
+                k = len(info.targets)
+                for s in range(1 << k):
+                    zm = 0
+                    for j in range(k):  # walsh index bit j <-> targets[k-1-j] (msb = targets[0])
+                        if s >> j & 1:
+                            zm |= 1 << info.targets[k - 1 - j]
+                    col = self.angle_col(1, info.const_col + s, 0.0)
+                    out.append((zm, col, 0.0))
+        return out
+
+    def new_slot(self) -> int:
+        self.n_slots += 1
+        return self.n_slots - 1
+
+
+def _walsh_angles(diag_entries: np.ndarray) -> np.ndarray:
+    """Angles a_s (s over subsets of local bits, bit j <-> local bit j from the LSB) with
+    diag[x] = exp(-i sum_s a_s (-1)^{popc(s & x)})."""
+    phi = -np.angle(diag_entries)
+    d = phi.shape[-1]
+    a = phi.copy()
+    h = 1
+    while h < d:
+        for i in range(0, d, 2 * h):
+            x = a[..., i:i + h].copy()
+            y = a[..., i + h:i + 2 * h].copy()
+            a[..., i:i + h] = x + y
+            a[..., i + h:i + 2 * h] = x - y
+        h *= 2
+    return a / d
+
+
+def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool,
+                  observables=None, obs_diag_ids=(), lam_diag: bool = False) -> Program:
+    """Plan + emit.  ``observables``: list of PauliSums; ``obs_diag_ids``: those fused as
+    OBS ops at the end of the forward program; ``lam_diag``: adjoint with a diagonal H
+    whose lambda-init / energy is fused into the first backward pass."""
+    L, R = (ADJ_L, ADJ_R) if adjoint else (FWD_L, FWD_R)
+    L = min(L, n)
+    ops = build_ops(infos, adjoint)
+    ops, init = absorb_product_init(ops, infos, n, allow_symbolic=not adjoint)
+    # observable ops
+    obs_ops = []
+    if not adjoint:
+        for oid in obs_diag_ids:
+            obs_ops.append(Op(OP_OBS, tuple(range(n)), obs=oid))
+    passes = plan_passes(ops, n, L)
+    for p in passes:
+        plan_stages(p, R)
+    if obs_ops:
+        passes[-1].stages[-1].ops.extend(obs_ops)
+    if adjoint and lam_diag:
+        obs_ops = [Op(OP_OBS, tuple(range(n)), obs=0)]
+
+    em = Emitter(n, L, R, infos, adjoint)
+    # -- generator / fixed tables for the build recipe
+    gen_rows = []
+    n_fixed = 0
+    n_const = 0
+    for info in infos:
+        if info.symbolic:
+            info.gen = len(gen_rows)
+            gen_rows.append(info)
+        elif info.diag:
+            info.const_col = n_const
+            n_const += 1 << len(info.targets)
+        else:
+            info.fixed = n_fixed
+            n_fixed += 1
+
+    seq = list(passes)
+    if adjoint:
+        seq = list(reversed(passes))
+    for pi, p in enumerate(seq):
+        first_fwd = p is passes[0]
+        last_fwd = p is passes[-1]
+        stages = list(reversed(p.stages)) if adjoint else list(p.stages)
+        prow = np.zeros(PASS_INTS, dtype=np.int32)
+        prow[0] = len(em.stage_rows)
+        if adjoint:
+            prow[2] = (INIT_LOAD_PSI if lam_diag else INIT_LOAD) if last_fwd else INIT_LOAD
+            prow[3] = 0 if first_fwd else 1
+        else:
+            prow[2] = (INIT_PRODUCT if init else INIT_ZERO) if first_fwd else INIT_LOAD
+            prow[3] = 1
+        prow[4] = em.n_mat
+        prow[6] = em.n_ang
+        prow[8] = em.n_slots
+        prow[11] = em.n_coef
+        prow[13] = L
+        outer = [q for q in range(n) if q not in set(p.qubits)]
+        prow[10] = len(outer)
+        prow[16:16 + len(outer)] = outer
+        prow[48:80] = -1
+        if not adjoint and first_fwd:
+            for q, op in sorted(init.items()):
+                prow[48 + q] = em.dense_mat(op, (q,))
+        for si, st in enumerate(stages):
+            regs, thr = stage_slots(p, st, R)
+            srow = np.zeros(STAGE_INTS, dtype=np.int32)
+            reg_glob = [p.qubits[b] for b in regs]
+            srow[0:R] = reg_glob
+            srow[8:8 + len(thr)] = [p.qubits[b] for b in thr]
+            srow[24:24 + R] = [swizzle(1 << b) for b in regs]
+            srow[32:32 + len(thr)] = [swizzle(1 << b) for b in thr]
+            srow[48] = len(em.op_rows)
+            slot_of = {q: j for j, q in enumerate(reg_glob)}
+            st_ops = list(reversed(st.ops)) if adjoint else list(st.ops)
+            if adjoint and lam_diag and last_fwd and si == 0:
+                st_ops = obs_ops + st_ops
+            for op in st_ops:
+                orow = np.full(OP_INTS, 0, dtype=np.int32)
+                orow[0] = op.kind
+                orow[7] = -1
+                orow[8] = -1
+                if op.kind in (OP_DENSE1, OP_DENSE2):
+                    if op.kind == OP_DENSE1:
+                        order = (op.qubits[0],)
+                        orow[1] = slot_of[op.qubits[0]]
+                    else:
+                        a, b = op.qubits
+                        order = (a, b) if slot_of[a] < slot_of[b] else (b, a)
+                        orow[1], orow[2] = slot_of[order[0]], slot_of[order[1]]
+                    orow[3] = em.dense_mat(op, order)
+                    if adjoint and op.symbolic:
+                        (gi,) = op.factors
+                        info = infos[gi]
+                        gm, _ = generator_matrix_from_terms(info.terms, order)
+                        gm = gm * (2.0 * info.coeff)
+                        orow[8] = len(em.genmats) // 2
+                        em.genmats.extend(np.stack([gm.real, gm.imag], -1).reshape(-1).tolist())
+                        orow[7] = em.new_slot()
+                        em.grad_slots.setdefault(info.sym, []).append(int(orow[7]))
+                elif op.kind == OP_DIAG:
+                    terms = em.diag_terms(op)
+                    b_, e_, g_ = em.emit_terms(terms, reg_glob)
+                    orow[4], orow[5], orow[6] = b_, e_, g_
+                    if adjoint and op.symbolic:
+                        orow[7] = em.new_slot()
+                        em.grad_slots.setdefault(op.sym, []).append(int(orow[7]))
+                elif op.kind == OP_OBS:
+                    obs = observables[op.obs]
+                    terms = []
+                    for ti, t in enumerate(obs.terms):
+                        xm, zm, ny = term_masks(t)
+                        assert xm == 0
+                        terms.append((zm, em.n_coef, 0.0))
+                        em.coef_cols.append((op.obs, ti))
+                        em.n_coef += 1
+                    b_, e_, g_ = em.emit_terms(terms, reg_glob)
+                    orow[4], orow[5], orow[6] = b_, e_, g_
+                    orow[7] = em.new_slot()
+                    if adjoint:
+                        em.energy_slots.append(int(orow[7]))
+                    else:
+                        em.obs_slots.setdefault(op.obs, []).append(int(orow[7]))
+                em.op_rows.append(orow)
+            srow[49] = len(em.op_rows)
+            em.stage_rows.append(srow)
+        prow[1] = len(em.stage_rows)
+        prow[5] = em.n_mat
+        prow[7] = em.n_ang
+        prow[9] = em.n_slots
+        prow[12] = em.n_coef
+        em.pass_rows.append(prow)
+
+    # build recipe arrays
+    gen_sym = np.array([g.sym for g in gen_rows], dtype=np.int32)
+    gen_coeff = np.array([g.coeff for g in gen_rows], dtype=np.float64)
+    gen_const = np.array([g.const for g in gen_rows], dtype=np.float64)
+    gen_dim = np.array([1 << len(g.targets) for g in gen_rows], dtype=np.int32)
+    gen_eval = np.zeros((len(gen_rows), 4))
+    gen_evec = np.zeros((len(gen_rows), 4, 4), dtype=np.complex128)
+    for k, g in enumerate(gen_rows):
+        h = np.zeros((1 << len(g.targets),) * 2, dtype=np.complex128)
+        for f, c in g.terms:
+            h += _pauli_local(f, c, g.targets)
+        w, v = np.linalg.eigh(h)
+        d = len(w)
+        gen_eval[k, :d] = w
+        gen_evec[k, :d, :d] = v
+    fbeg = [0]
+    flat = []
+    dmat, ddim = [], []
+    for off, d, facs in em.dense_recipe:
+        dmat.append(off)
+        ddim.append(d)
+        for f in facs:
+            flat.extend(f)
+        fbeg.append(len(flat) // 3)
+    tsrc = np.array([(k, s) for k, s, _ in em.term_src], dtype=np.int32).reshape(-1, 2)
+    tbeta = np.array([b for _, _, b in em.term_src], dtype=np.float64)
+    recipe = dict(
+        gen_sym=gen_sym, gen_coeff=gen_coeff, gen_const=gen_const, gen_dim=gen_dim,
+        gen_eval=gen_eval.reshape(-1), gen_evec=np.stack([gen_evec.real, gen_evec.imag], -1).reshape(-1),
+        n_fixed=n_fixed, n_const=n_const,
+        dense_mat=np.array(dmat, dtype=np.int32), dense_dim=np.array(ddim, dtype=np.int32),
+        dense_fbeg=np.array(fbeg, dtype=np.int32), factor=np.array(flat, dtype=np.int32),
+        term_src=tsrc.reshape(-1), term_beta=tbeta,
+    )
+    stats = dict(passes=len(passes), stages=len(em.stage_rows), ops=len(em.op_rows),
+                 stages_per_pass=[len(p.stages) for p in passes],
+                 ops_per_pass=[len(p.ops) for p in passes], product_init=len(init),
+                 tile_qubits=[p.qubits for p in passes])
+    return Program(
+        n=n, L=L, R=R, adjoint=adjoint,
+        passes=np.array(em.pass_rows, dtype=np.int32).reshape(-1, PASS_INTS),
+        stages=np.array(em.stage_rows, dtype=np.int32).reshape(-1, STAGE_INTS),
+        ops=np.array(em.op_rows, dtype=np.int32).reshape(-1, OP_INTS),
+        term_mask=np.array(em.term_mask, dtype=np.uint32),
+        term_idx=np.array(em.term_idx, dtype=np.int32),
+        term_w=np.array(em.term_w, dtype=np.float32),
+        grp=np.array(em.grp, dtype=np.int32),
+        genmats=np.array(em.genmats, dtype=np.float32),
+        n_slots=em.n_slots, n_mat=em.n_mat, n_ang=em.n_ang, n_coef=em.n_coef,
+        recipe=recipe, grad_slots=em.grad_slots, obs_slots=em.obs_slots,
+        energy_slots=em.energy_slots, stats=stats,
+    )
+
+
+_PAULI = {
+    "X": np.array([[0, 1], [1, 0]], dtype=np.complex128),
+    "Y": np.array([[0, -1j], [1j, 0]], dtype=np.complex128),
+    "Z": np.array([[1, 0], [0, -1]], dtype=np.complex128),
+    "I": np.eye(2, dtype=np.complex128),
+}
+
+
+def _pauli_local(factors, coef, order):
+    m = np.array([[coef]], dtype=np.complex128)
+    for q in order:
+        m = np.kron(m, _PAULI[factors.get(q, "I")])
+    return m
+
+
+def generator_matrix_from_terms(terms, order):
+    """(non-identity part of the generator in local basis ``order``, identity coefficient)."""
+    d = 1 << len(order)
+    h = np.zeros((d, d), dtype=np.complex128)
+    ident = 0.0
+    for f, c in terms:
+        if not f:
+            ident += c
+        else:
+            h += _pauli_local(f, c, order)
+    return h, ident
+
+
+# ---------------------------------------------------------------------------
+# per-row values of concrete gates
+# ---------------------------------------------------------------------------
+
+_MAT_CACHE: dict = {}
+
+
+def concrete_matrix(g) -> np.ndarray:
+    hit = _MAT_CACHE.get(id(g))
+    if hit is not None and hit[0] is g:
+        return hit[1]
+    m = np.asarray(gate_matrix(g), dtype=np.complex128)
+    if len(_MAT_CACHE) > 200_000:
+        _MAT_CACHE.clear()
+    _MAT_CACHE[id(g)] = (g, m)
+    return m
+
+
+def concrete_tables(circuits, infos):
+    """fixed [Bf, n_fixed, 16] complex128 (4x4-stride) and const angles [Bc, n_const]."""
+    fixed_pos = [i for i in infos if not i.symbolic and not i.diag]
+    diag_pos = [i for i in infos if not i.symbolic and i.diag]
+    n_fixed = len(fixed_pos)
+    n_const = sum(1 << len(i.targets) for i in diag_pos)
+    shared = all(c is circuits[0] for c in circuits) or len(circuits) == 1
+    if not shared:
+        shared = True
+        for info in fixed_pos + diag_pos:
+            g0 = circuits[0].gates[info.index]
+            if any(c.gates[info.index] is not g0 for c in circuits[1:]):
+                shared = False
+                break
+    rows = circuits[:1] if shared else circuits
+    fixed = np.zeros((len(rows), max(n_fixed, 1), 4, 4), dtype=np.complex128)
+    consts = np.zeros((len(rows), max(n_const, 1)), dtype=np.float64)
+    for r, c in enumerate(rows):
+        for info in fixed_pos:
+            m = concrete_matrix(c.gates[info.index])
+            d = m.shape[0]
+            fixed[r, info.fixed, :d, :d] = m
+        for info in diag_pos:
+            m = concrete_matrix(c.gates[info.index])
+            k = len(info.targets)
+            consts[r, info.const_col:info.const_col + (1 << k)] = _walsh_angles(np.diag(m))
+    return fixed, consts
