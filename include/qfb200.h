@@ -34,6 +34,7 @@ extern "C" {
 /* ---- device program descriptors (all-int32 layouts, mirrored in planner.py) ---- */
 
 #define QF_MAX_R 8
+#define QF_LANE_Q 4   /* qubits 0..3 are lane bits at every load/store */
 #define QF_MAX_T 16
 #define QF_MAX_Q 40
 
@@ -62,7 +63,9 @@ typedef struct QfOp {
   int32_t grp;                   /* DIAG/OBS: offset of the 2^R+1 subset-boundary table */
   int32_t slot;                  /* gradient / expectation slot, -1 = none */
   int32_t gen;                   /* ADJ dense gradient: generator matrix offset (complex units) */
-  int32_t pad[7];
+  int32_t cls;                   /* DENSE1 matrix class: 0 general, 1 [[a,ib],[ic,d]], 2 real */
+  int32_t gkind;                 /* ADJ DENSE1 generator: 0 matrix, 1 X, 2 Y, 3 Z (scale = complex genmats[gen + 4].x) */
+  int32_t pad[5];
 } QfOp;                          /* 16 x int32 */
 
 typedef struct QfPass {
@@ -74,10 +77,12 @@ typedef struct QfPass {
   int32_t n_outer;
   int32_t coef_begin, coef_end;  /* observable coefficient columns */
   int32_t L;
-  int32_t pad0[2];
+  int32_t term_begin, term_end;  /* phase-polynomial / observable terms of this pass */
   int32_t outer_pos[32];         /* global positions of the n-L non-tile bits */
   int32_t init_mat[32];          /* product init: matrix offset of qubit q's leading 2x2, -1 = |0> */
-  int32_t pad1[48];
+  int32_t grp_begin, grp_end;    /* subset-boundary tables of this pass */
+  int32_t op_begin, op_end;      /* ops of this pass */
+  int32_t pad1[44];
 } QfPass;                        /* 128 x int32 */
 
 /* Everything one pass launch needs; pointers are device pointers. */

@@ -3,40 +3,83 @@
 // targets lie inside the tile's qubit set Q (|Q| = L, Q contains qubits 0..4 so
 // every warp-wide global access is 256 contiguous bytes).  Within a pass the
 // planner splits the op list into stages; each stage has a register mapping
-// (which tile bits live in registers) and stages are connected by one
-// swizzled shared-memory transpose.  Diagonal gates are phase polynomials and
-// run in any stage without data movement.
+// (which tile bits live in registers) and consecutive stages are connected by one
+// swizzled shared-memory transpose.  Diagonal gates are phase polynomials
+// evaluated from the amplitude index (integer Walsh-Hadamard transform over the
+// register bits) and need no data movement.
 //
-// Reference semantics being accelerated: qcflow/sim.py:88-136 (apply_matrix /
-// run_ops), sim.py:177-213 (Pauli expectation), gradients.py (the adjoint here
-// replaces the parameter-shift loop, oracle = PS).
+// Reference semantics accelerated here: qcflow/sim.py:88-136 (apply_matrix /
+// run_ops), sim.py:177-213 (Pauli expectation); the ADJ instantiation is the
+// adjoint differentiator whose oracle is gradients.py:158-165 / :241-326.
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <utility>
 
 #include "qf_common.cuh"
 
 namespace qf {
 
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  [&]<int... I>(std::integer_sequence<int, I...>) {
+    (f(std::integral_constant<int, I>{}), ...);
+  }(std::make_integer_sequence<int, N>{});
+}
+
+// Visit the 2^R register indices in Gray-code order with a running XOR offset
+// (consecutive Gray codes differ in one bit -> one LOP per amplitude).
+template <int R, typename F>
+__device__ __forceinline__ void gray_walk(uint32_t base, const uint32_t (&step)[R], F&& f) {
+  uint32_t off = base;
+  static_for<(1 << R)>([&](auto I) {
+    constexpr int i = decltype(I)::value;
+    if constexpr (i != 0) {
+      constexpr int j = ctz_c(i);
+      off ^= step[j];
+    }
+    f(std::integral_constant<int, gray_c(i)>{}, off);
+  });
+}
 
 // ---------------------------------------------------------------------------
 // dense gates on register slots (compile-time slots, runtime matrices in smem)
 // ---------------------------------------------------------------------------
 
-template <int J, int NR>
-__device__ __forceinline__ void apply1(float2 (&v)[NR], const float2* __restrict__ u, bool adj) {
-  float2 u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
-  if (adj) {  // U^dagger
-    float2 t = u01;
-    u00.y = -u00.y; u11.y = -u11.y;
-    u01 = make_float2(u10.x, -u10.y);
-    u10 = make_float2(t.x, -t.y);
-  }
+// U (2x2) on register slot J; CLS selects the arithmetic for the matrix structure
+// (0 general complex, 1 [[a, ib], [ic, d]], 2 real) -- 4 / 2 / 2 FP32x2 ops per amplitude.
+template <int J, int NR, int CLS>
+__device__ __forceinline__ void apply1(float2 (&v)[NR], float2 u00, float2 u01, float2 u10, float2 u11) {
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
     if (r & (1 << J)) continue;
-    float2 a = v[r], b = v[r | (1 << J)];
-    v[r] = cmad2(u00, a, u01, b);
-    v[r | (1 << J)] = cmad2(u10, a, u11, b);
+    const float2 a = v[r], b = v[r | (1 << J)];
+    if constexpr (CLS == 0) {
+      v[r] = cmad2(u00, a, u01, b);
+      v[r | (1 << J)] = cmad2(u10, a, u11, b);
+    } else if constexpr (CLS == 1) {
+      v[r] = xrow(u00.x, a, u01.y, b);
+      v[r | (1 << J)] = xrow(u11.x, b, u10.y, a);
+    } else {
+      v[r] = rrow(u00.x, a, u01.x, b);
+      v[r | (1 << J)] = rrow(u10.x, a, u11.x, b);
+    }
+  }
+}
+
+// load a 2x2 from smem, optionally as its conjugate transpose
+__device__ __forceinline__ void load_u2(const float2* u, bool adj, float2& u00, float2& u01, float2& u10,
+                                        float2& u11) {
+  u00 = u[0];
+  u01 = u[1];
+  u10 = u[2];
+  u11 = u[3];
+  if (adj) {
+    const float2 t = u01;
+    u00.y = -u00.y;
+    u11.y = -u11.y;
+    u01 = make_float2(u10.x, -u10.y);
+    u10 = make_float2(t.x, -t.y);
   }
 }
 
@@ -55,14 +98,13 @@ __device__ __forceinline__ void apply2(float2 (&v)[NR], const float2* __restrict
   for (int r = 0; r < NR; ++r) {
     if (r & ((1 << J0) | (1 << J1))) continue;
     const int i0 = r, i1 = r | (1 << J1), i2 = r | (1 << J0), i3 = r | (1 << J0) | (1 << J1);
-    float2 a0 = v[i0], a1 = v[i1], a2 = v[i2], a3 = v[i3];
+    const float2 a0 = v[i0], a1 = v[i1], a2 = v[i2], a3 = v[i3];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       float2 o = cmad2(m[i * 4 + 0], a0, m[i * 4 + 1], a1);
-      float2 p = cmad2(m[i * 4 + 2], a2, m[i * 4 + 3], a3);
-      o.x += p.x; o.y += p.y;
-      const int dst = i == 0 ? i0 : i == 1 ? i1 : i == 2 ? i2 : i3;
-      v[dst] = o;
+      o = cfma(m[i * 4 + 2], a2, o);
+      o = cfma(m[i * 4 + 3], a3, o);
+      v[i == 0 ? i0 : i == 1 ? i1 : i == 2 ? i2 : i3] = o;
     }
   }
 }
@@ -76,9 +118,28 @@ __device__ __forceinline__ float grad1(const float2 (&p)[NR], const float2 (&l)[
   for (int r = 0; r < NR; ++r) {
     if (r & (1 << J)) continue;
     const int r1 = r | (1 << J);
-    float2 t0 = cmad2(g00, p[r], g01, p[r1]);
-    float2 t1 = cmad2(g10, p[r], g11, p[r1]);
+    const float2 t0 = cmad2(g00, p[r], g01, p[r1]);
+    const float2 t1 = cmad2(g10, p[r], g11, p[r1]);
     acc += im_conj_mul(l[r], t0) + im_conj_mul(l[r1], t1);
+  }
+  return acc;
+}
+
+// Im <lam| c P |psi> for a single Pauli P on slot J (GK 1 = X, 2 = Y, 3 = Z); c applied by the caller.
+template <int J, int NR, int GK>
+__device__ __forceinline__ float gradp(const float2 (&p)[NR], const float2 (&l)[NR]) {
+  float acc = 0.f;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    if (r & (1 << J)) continue;
+    const int r1 = r | (1 << J);
+    if constexpr (GK == 1) {
+      acc += im_conj_mul(l[r], p[r1]) + im_conj_mul(l[r1], p[r]);
+    } else if constexpr (GK == 2) {
+      acc += re_conj_mul(l[r1], p[r]) - re_conj_mul(l[r], p[r1]);
+    } else {
+      acc += im_conj_mul(l[r], p[r]) - im_conj_mul(l[r1], p[r1]);
+    }
   }
   return acc;
 }
@@ -93,8 +154,9 @@ __device__ __forceinline__ float grad2(const float2 (&p)[NR], const float2 (&l)[
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       float2 t = cmad2(g[i * 4 + 0], p[idx[0]], g[i * 4 + 1], p[idx[1]]);
-      float2 u = cmad2(g[i * 4 + 2], p[idx[2]], g[i * 4 + 3], p[idx[3]]);
-      t.x += u.x; t.y += u.y;
+      const float2 u = cmad2(g[i * 4 + 2], p[idx[2]], g[i * 4 + 3], p[idx[3]]);
+      t.x += u.x;
+      t.y += u.y;
       acc += im_conj_mul(l[idx[i]], t);
     }
   }
@@ -117,8 +179,8 @@ __device__ __forceinline__ void dispatch1(int s, Fn&& fn) {
 
 template <int R, typename Fn>
 __device__ __forceinline__ void dispatch2(int s0, int s1, Fn&& fn) {
-#define QF_P(A, B)                                                         \
-  case A * 8 + B:                                                          \
+#define QF_P(A, B)                                                \
+  case A * 8 + B:                                                 \
     if constexpr (A < R && B < R) fn.template operator()<A, B>(); \
     break;
   switch (s0 * 8 + s1) {
@@ -136,82 +198,78 @@ __device__ __forceinline__ void dispatch2(int s0, int s1, Fn&& fn) {
 // stage geometry
 // ---------------------------------------------------------------------------
 
-template <int R, int TB>
-__device__ __forceinline__ uint32_t thread_bits(const QfStage& st, int t, bool phys) {
+// XOR of per-thread-bit contributions (global bit positions or swizzled smem offsets).
+template <int TB>
+__device__ __forceinline__ uint32_t thread_glob(const QfStage& st, int t) {
   uint32_t x = 0;
 #pragma unroll
   for (int i = 0; i < TB; ++i)
-    if (t & (1 << i)) x ^= phys ? (uint32_t)st.thr_phys[i] : (1u << st.thr_glob[i]);
+    if (t & (1 << i)) x ^= 1u << st.thr_glob[i];
+  return x;
+}
+template <int TB>
+__device__ __forceinline__ uint32_t thread_phys(const QfStage& st, int t) {
+  uint32_t x = 0;
+#pragma unroll
+  for (int i = 0; i < TB; ++i)
+    if (t & (1 << i)) x ^= (uint32_t)st.thr_phys[i];
   return x;
 }
 
 // write v (mapping `from`) to smem, read back with mapping `to`.
 template <int R, int TB, int NA>
-__device__ __forceinline__ void remap(float2 (&v)[NA][1 << R], float2* sm, int tile_elems,
-                                      const QfStage& from, const QfStage& to, int t) {
-  constexpr int NR = 1 << R;
+__device__ __forceinline__ void remap(float2 (&v)[NA][1 << R], float2* sm, const QfStage& from,
+                                      const QfStage& to, int t) {
+  constexpr int TILE = 1 << (R + TB);
+  uint32_t ph[R];
   __syncthreads();
-  {
-    const uint32_t base = thread_bits<R, TB>(from, t, true);
-    uint32_t ph[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) ph[j] = (uint32_t)from.reg_phys[j];
-    uint32_t addr = base;
+  for (int j = 0; j < R; ++j) ph[j] = (uint32_t)from.reg_phys[j];
+  gray_walk<R>(thread_phys<TB>(from, t), ph, [&](auto r, uint32_t addr) {
 #pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      if (i) addr ^= ph[ctz_c(i)];
-#pragma unroll
-      for (int a = 0; a < NA; ++a) sm[a * tile_elems + addr] = v[a][gray_c(i)];
-    }
-  }
+    for (int q = 0; q < NA; ++q) sm[q * TILE + addr] = v[q][decltype(r)::value];
+  });
   __syncthreads();
-  {
-    const uint32_t base = thread_bits<R, TB>(to, t, true);
-    uint32_t ph[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) ph[j] = (uint32_t)to.reg_phys[j];
-    uint32_t addr = base;
+  for (int j = 0; j < R; ++j) ph[j] = (uint32_t)to.reg_phys[j];
+  gray_walk<R>(thread_phys<TB>(to, t), ph, [&](auto r, uint32_t addr) {
 #pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      if (i) addr ^= ph[ctz_c(i)];
-#pragma unroll
-      for (int a = 0; a < NA; ++a) v[a][gray_c(i)] = sm[a * tile_elems + addr];
-    }
-  }
+    for (int q = 0; q < NA; ++q) v[q][decltype(r)::value] = sm[q * TILE + addr];
+  });
 }
 
-// A[S] = sum_{k: subset(k) = S} sign_k(t) * value_k  (subset tables built by the planner)
+// A[S] = sum_{k: subset(k) = S} (-1)^{popc(gt & mask_k)} * value_k
+// grp: smem subset-boundary table (2^R + 1 entries, pass-relative term indices).
 template <int R, typename T, typename ValFn>
-__device__ __forceinline__ void subset_accumulate(T (&A)[1 << R], const QfProgram& P, const QfOp& op,
+__device__ __forceinline__ void subset_accumulate(T (&A)[1 << R], const int32_t* grp, const uint2* terms,
                                                   uint32_t gt, ValFn&& val) {
-  const int32_t* grp = P.grp + op.grp;
-#pragma unroll
-  for (int S = 0; S < (1 << R); ++S) {
+  static_for<(1 << R)>([&](auto SI) {
+    constexpr int S = decltype(SI)::value;
     T acc = T(0);
-    const int kb = __ldg(grp + S), ke = __ldg(grp + S + 1);
+    const int kb = grp[S], ke = grp[S + 1];
     for (int k = kb; k < ke; ++k) {
-      const uint32_t m = __ldg(P.term_mask + k);
-      const T x = val(k);
-      acc = (__popc(gt & m) & 1) ? acc - x : acc + x;
+      const uint2 tm = terms[k];
+      const T x = val(tm, k);
+      acc = (__popc(gt & tm.x) & 1) ? acc - x : acc + x;
     }
     A[S] = acc;
-  }
+  });
 }
 
 // ---------------------------------------------------------------------------
-// forward pass kernel
+// the pass kernel
 // ---------------------------------------------------------------------------
 
-struct SmemLayout {
-  int tile;   // float2 elements of one tile
-  int mats;   // float2 elements
-  int angs;   // int32
-  int coefs;  // float
-  int slots;  // float
+template <int L, int R, bool ADJ>
+struct KTraits {
+  static constexpr int NT = 1 << (L - R);
+  // forward tiles of 8192 amplitudes fit two CTAs per SM at <=128 registers
+  // at most 128 registers per thread: 65536 / (threads * 128) resident CTAs per SM
+  static constexpr int MINB = (65536 / (NT * 128)) > 8 ? 8 : (65536 / (NT * 128));
 };
 
 template <int L, int R, bool ADJ>
-__global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
+__global__ void __launch_bounds__(KTraits<L, R, ADJ>::NT, KTraits<L, R, ADJ>::MINB) pass_kernel(const PassArgs a) {
   constexpr int NR = 1 << R;
   constexpr int TB = L - R;
   constexpr int NT = 1 << TB;
@@ -220,70 +278,89 @@ __global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
 
   const QfProgram& P = a.prog;
-  const QfPass& pass = P.passes[a.pass];
+  const QfPass* gpass = P.passes + a.pass;
   const int t = threadIdx.x;
   const int tiles_log2 = a.tiles_log2;
   const int row = (int)(blockIdx.x >> tiles_log2);
   const uint32_t o = blockIdx.x & ((1u << tiles_log2) - 1u);
 
-  const int mat_begin = pass.mat_begin, mat_cnt = pass.mat_end - pass.mat_begin;
-  const int ang_begin = pass.ang_begin, ang_cnt = pass.ang_end - pass.ang_begin;
-  const int coef_begin = pass.coef_begin, coef_cnt = pass.coef_end - pass.coef_begin;
-  const int slot_begin = pass.slot_begin, slot_cnt = pass.slot_end - pass.slot_begin;
+  const int mat_begin = gpass->mat_begin, mat_cnt = gpass->mat_end - mat_begin;
+  const int term_begin = gpass->term_begin, term_cnt = gpass->term_end - term_begin;
+  const int grp_begin = gpass->grp_begin, grp_cnt = gpass->grp_end - grp_begin;
+  const int op_begin = gpass->op_begin, op_cnt = gpass->op_end - op_begin;
+  const int st_begin = gpass->stage_begin, st_cnt = gpass->stage_end - st_begin;
+  const int slot_begin = gpass->slot_begin, slot_cnt = gpass->slot_end - slot_begin;
 
+  // ---- shared memory carve-up ----
   float2* tile = reinterpret_cast<float2*>(smem_raw);
-  float2* msm = tile + NA * TILE;
-  int32_t* asm_ = reinterpret_cast<int32_t*>(msm + mat_cnt);
-  float* csm = reinterpret_cast<float*>(asm_ + ang_cnt);
-  double* ssm = reinterpret_cast<double*>(reinterpret_cast<uintptr_t>(csm + coef_cnt + 1) & ~uintptr_t(7));
+  QfStage* sst = reinterpret_cast<QfStage*>(tile + NA * TILE);
+  QfOp* sop = reinterpret_cast<QfOp*>(sst + st_cnt);
+  double* ssm = reinterpret_cast<double*>(sop + op_cnt);
+  float2* msm = reinterpret_cast<float2*>(ssm + slot_cnt);
+  uint2* stm = reinterpret_cast<uint2*>(msm + mat_cnt);
+  float* stw = reinterpret_cast<float*>(stm + term_cnt);
+  int32_t* sgr = reinterpret_cast<int32_t*>(stw + (ADJ ? term_cnt : 0));
 
-  // per-row constants of this pass -> smem
   {
+    const int32_t* s32 = reinterpret_cast<const int32_t*>(P.stages + st_begin);
+    int32_t* d32 = reinterpret_cast<int32_t*>(sst);
+    for (int i = t; i < st_cnt * 64; i += NT) d32[i] = s32[i];
+    s32 = reinterpret_cast<const int32_t*>(P.ops + op_begin);
+    d32 = reinterpret_cast<int32_t*>(sop);
+    for (int i = t; i < op_cnt * 16; i += NT) d32[i] = s32[i];
+    for (int i = t; i < slot_cnt; i += NT) ssm[i] = 0.0;
     const float2* src = a.mats + (size_t)row * P.n_mat + mat_begin;
     for (int i = t; i < mat_cnt; i += NT) msm[i] = src[i];
-    const int32_t* as = a.angles + (size_t)row * P.n_ang + ang_begin;
-    for (int i = t; i < ang_cnt; i += NT) asm_[i] = as[i];
-    const float* cs = a.coefs + (size_t)row * P.coef_row_stride + coef_begin;
-    for (int i = t; i < coef_cnt; i += NT) csm[i] = cs[i];
-    for (int i = t; i < slot_cnt; i += NT) ssm[i] = 0.0;
+    const int32_t* arow = a.angles + (size_t)row * P.n_ang;
+    const float* crow = a.coefs + (size_t)row * P.coef_row_stride;
+    for (int i = t; i < term_cnt; i += NT) {
+      const int k = term_begin + i;
+      const int idx = P.term_idx[k];
+      // DIAG terms index the angle table, OBS terms the coefficient table; the planner
+      // marks OBS columns with a negative index (-1 - column).
+      const int32_t val = idx >= 0 ? arow[idx] : __float_as_int(crow[-1 - idx]);
+      stm[i] = make_uint2(P.term_mask[k], (uint32_t)val);
+      if constexpr (ADJ) stw[i] = P.term_w[k];
+    }
+    for (int i = t; i < grp_cnt; i += NT) sgr[i] = P.grp[grp_begin + i] - term_begin;
   }
 
   // global bits of this tile's outer index
   uint32_t base = 0;
-  for (int i = 0; i < pass.n_outer; ++i)
-    if (o & (1u << i)) base |= 1u << pass.outer_pos[i];
+  {
+    const int nout = gpass->n_outer;
+    for (int i = 0; i < nout; ++i)
+      if (o & (1u << i)) base |= 1u << gpass->outer_pos[i];
+  }
+  const int init = gpass->init, store = gpass->store;
 
   const size_t row_elems = (size_t)1 << a.n;
   float2* psi_row = a.psi + (size_t)row * row_elems;
   float2* lam_row = ADJ ? a.lam + (size_t)row * row_elems : nullptr;
 
   float2 v[NA][NR];
-  const QfStage* st0 = P.stages + pass.stage_begin;
   __syncthreads();
 
-  // ---- load / initialise ----
+  // ---- load / initialise (stage 0 mapping; lanes sit on qubits 0..4) ----
   {
-    const uint32_t gt = base | thread_bits<R, TB>(*st0, t, false);
+    const QfStage& st0 = sst[0];
+    const uint32_t gt = base | thread_glob<TB>(st0, t);
     uint32_t rg[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) rg[j] = 1u << st0->reg_glob[j];
-    if (pass.init == QF_INIT_LOAD || pass.init == QF_INIT_LOAD_PSI) {
-      const bool with_lam = ADJ && pass.init == QF_INIT_LOAD;
-      uint32_t g = gt;
-#pragma unroll
-      for (int i = 0; i < NR; ++i) {
-        if (i) g ^= rg[ctz_c(i)];
-        v[0][gray_c(i)] = psi_row[g];
-        if constexpr (ADJ) v[1][gray_c(i)] = with_lam ? lam_row[g] : make_float2(0.f, 0.f);
-      }
-    } else if (pass.init == QF_INIT_ZERO) {
-      uint32_t g = gt;
-#pragma unroll
-      for (int i = 0; i < NR; ++i) {
-        if (i) g ^= rg[ctz_c(i)];
-        v[0][gray_c(i)] = make_float2(g == 0 ? 1.f : 0.f, 0.f);
-        if constexpr (ADJ) v[1][gray_c(i)] = make_float2(0.f, 0.f);
-      }
+    for (int j = 0; j < R; ++j) rg[j] = 1u << st0.reg_glob[j];
+    if (init == QF_INIT_LOAD || init == QF_INIT_LOAD_PSI) {
+      const bool with_lam = ADJ && init == QF_INIT_LOAD;
+      gray_walk<R>(gt, rg, [&](auto r, uint32_t g) {
+        constexpr int ri = decltype(r)::value;
+        v[0][ri] = psi_row[g];
+        if constexpr (ADJ) v[1][ri] = with_lam ? lam_row[g] : make_float2(0.f, 0.f);
+      });
+    } else if (init == QF_INIT_ZERO) {
+      gray_walk<R>(gt, rg, [&](auto r, uint32_t g) {
+        constexpr int ri = decltype(r)::value;
+        v[0][ri] = make_float2(g == 0 ? 1.f : 0.f, 0.f);
+        if constexpr (ADJ) v[1][ri] = make_float2(0.f, 0.f);
+      });
     } else {  // product state: amp(x) = prod_q f_q[bit_q(x)], f_q = column 0 of qubit q's leading 2x2
       float2 c = make_float2(1.f, 0.f);
       uint32_t regmask = 0;
@@ -291,15 +368,15 @@ __global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
       for (int j = 0; j < R; ++j) regmask |= rg[j];
       for (int q = 0; q < a.n; ++q) {
         if (regmask & (1u << q)) continue;
-        const int mo = pass.init_mat[q];
+        const int mo = gpass->init_mat[q];
         const int bit = (gt >> q) & 1;
-        float2 f = mo < 0 ? make_float2(bit ? 0.f : 1.f, 0.f) : msm[mo - mat_begin + (bit ? 2 : 0)];
+        const float2 f = mo < 0 ? make_float2(bit ? 0.f : 1.f, 0.f) : msm[mo - mat_begin + (bit ? 2 : 0)];
         c = cmul(c, f);
       }
       v[0][0] = c;
 #pragma unroll
       for (int j = 0; j < R; ++j) {
-        const int mo = pass.init_mat[st0->reg_glob[j]];
+        const int mo = gpass->init_mat[st0.reg_glob[j]];
         const float2 f0 = mo < 0 ? make_float2(1.f, 0.f) : msm[mo - mat_begin];
         const float2 f1 = mo < 0 ? make_float2(0.f, 0.f) : msm[mo - mat_begin + 2];
 #pragma unroll
@@ -316,36 +393,48 @@ __global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
   }
 
   // ---- stages ----
-  float gacc = 0.f;  // per-op scalar accumulated over the warp before hitting smem
-  const int s_beg = pass.stage_begin, s_end = pass.stage_end;
-  for (int s = s_beg; s < s_end; ++s) {
-    const QfStage& st = P.stages[s];
-    if (s != s_beg) remap<R, TB, NA>(v, tile, TILE, P.stages[s - 1], st, t);
-    const uint32_t gt = base | thread_bits<R, TB>(st, t, false);
-    const int ob = st.op_begin, oe = st.op_end;
-    for (int k = 0; k < oe - ob; ++k) {
-      const QfOp op = P.ops[ob + k];  // ADJ programs are emitted in backward execution order
-      if (op.kind == QF_OP_DENSE1) {
-        const float2* u = msm + (op.mat - mat_begin);
+  for (int s = 0; s < st_cnt; ++s) {
+    const QfStage& st = sst[s];
+    if (s != 0) remap<R, TB, NA>(v, tile, sst[s - 1], st, t);
+    const uint32_t gt = base | thread_glob<TB>(st, t);
+    const int ob = st.op_begin - op_begin, oe = st.op_end - op_begin;
+    for (int k = ob; k < oe; ++k) {
+      const QfOp& op = sop[k];  // ADJ programs are emitted in backward execution order
+      const int kind = op.kind;
+      if (kind == QF_OP_DENSE1) {
+        float2 u00, u01, u10, u11;
+        load_u2(msm + (op.mat - mat_begin), ADJ, u00, u01, u10, u11);
+        const int cls = op.cls;
         if constexpr (ADJ) {
           if (op.slot >= 0) {
             const float2* g = reinterpret_cast<const float2*>(P.genmats) + op.gen;
-            dispatch1<R>(op.s0, [&]<int J>() { gacc = grad1<J, NR>(v[0], v[1], g); });
+            const int gk = op.gkind;
+            float gacc = 0.f;
+            dispatch1<R>(op.s0, [&]<int J>() {
+              if (gk == 1) gacc = gradp<J, NR, 1>(v[0], v[1]);
+              else if (gk == 2) gacc = gradp<J, NR, 2>(v[0], v[1]);
+              else if (gk == 3) gacc = gradp<J, NR, 3>(v[0], v[1]);
+              else gacc = grad1<J, NR>(v[0], v[1], g);
+            });
+            if (gk != 0) gacc *= g[4].x;
             const double gs = warp_sum_d((double)gacc);
             if ((t & 31) == 0) atomicAdd(ssm + (op.slot - slot_begin), gs);
           }
-          dispatch1<R>(op.s0, [&]<int J>() {
-            apply1<J, NR>(v[0], u, true);
-            apply1<J, NR>(v[1], u, true);
-          });
-        } else {
-          dispatch1<R>(op.s0, [&]<int J>() { apply1<J, NR>(v[0], u, false); });
         }
-      } else if (op.kind == QF_OP_DENSE2) {
+        dispatch1<R>(op.s0, [&]<int J>() {
+#pragma unroll
+          for (int q = 0; q < NA; ++q) {
+            if (cls == 1) apply1<J, NR, 1>(v[q], u00, u01, u10, u11);
+            else if (cls == 2) apply1<J, NR, 2>(v[q], u00, u01, u10, u11);
+            else apply1<J, NR, 0>(v[q], u00, u01, u10, u11);
+          }
+        });
+      } else if (kind == QF_OP_DENSE2) {
         const float2* u = msm + (op.mat - mat_begin);
         if constexpr (ADJ) {
           if (op.slot >= 0) {
             const float2* g = reinterpret_cast<const float2*>(P.genmats) + op.gen;
+            float gacc = 0.f;
             dispatch2<R>(op.s0, op.s1, [&]<int J0, int J1>() { gacc = grad2<J0, J1, NR>(v[0], v[1], g); });
             const double gs = warp_sum_d((double)gacc);
             if ((t & 31) == 0) atomicAdd(ssm + (op.slot - slot_begin), gs);
@@ -357,7 +446,8 @@ __global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
         } else {
           dispatch2<R>(op.s0, op.s1, [&]<int J0, int J1>() { apply2<J0, J1, NR>(v[0], u, false); });
         }
-      } else if (op.kind == QF_OP_DIAG) {
+      } else if (kind == QF_OP_DIAG) {
+        const int32_t* grp = sgr + (op.grp - grp_begin);
         if constexpr (ADJ) {
           if (op.slot >= 0) {
             float w[NR];
@@ -365,7 +455,7 @@ __global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
             for (int r = 0; r < NR; ++r) w[r] = im_conj_mul(v[1][r], v[0][r]);
             wht<R, float>(w);
             float W[NR];
-            subset_accumulate<R, float>(W, P, op, gt, [&](int k) { return __ldg(P.term_w + k); });
+            subset_accumulate<R, float>(W, grp, stm, gt, [&](uint2, int kk) { return stw[kk]; });
             float acc = 0.f;
 #pragma unroll
             for (int r = 0; r < NR; ++r) acc = fmaf(W[r], w[r], acc);
@@ -374,8 +464,7 @@ __global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
           }
         }
         uint32_t A[NR];
-        subset_accumulate<R, uint32_t>(A, P, op, gt,
-                                       [&](int k) { return (uint32_t)asm_[__ldg(P.term_idx + k) - ang_begin]; });
+        subset_accumulate<R, uint32_t>(A, grp, stm, gt, [&](uint2 tm, int) { return tm.y; });
         wht<R, uint32_t>(A);
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
@@ -383,9 +472,10 @@ __global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
 #pragma unroll
           for (int q = 0; q < NA; ++q) v[q][r] = cmul(v[q][r], ph);
         }
-      } else if (op.kind == QF_OP_OBS) {
+      } else if (kind == QF_OP_OBS) {
+        const int32_t* grp = sgr + (op.grp - grp_begin);
         float A[NR];
-        subset_accumulate<R, float>(A, P, op, gt, [&](int k) { return csm[__ldg(P.term_idx + k) - coef_begin]; });
+        subset_accumulate<R, float>(A, grp, stm, gt, [&](uint2 tm, int) { return __int_as_float((int)tm.y); });
         wht<R, float>(A);
         float e = 0.f;
 #pragma unroll
@@ -402,20 +492,18 @@ __global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
     }
   }
 
-  // ---- store ----
-  if (pass.store) {
-    const QfStage& st = P.stages[s_end - 1];
-    const uint32_t gt = base | thread_bits<R, TB>(st, t, false);
+  // ---- store (last stage mapping; lanes on qubits 0..4) ----
+  if (store) {
+    const QfStage& st = sst[st_cnt - 1];
+    const uint32_t gt = base | thread_glob<TB>(st, t);
     uint32_t rg[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) rg[j] = 1u << st.reg_glob[j];
-    uint32_t g = gt;
-#pragma unroll
-    for (int i = 0; i < NR; ++i) {
-      if (i) g ^= rg[ctz_c(i)];
-      psi_row[g] = v[0][gray_c(i)];
-      if constexpr (ADJ) lam_row[g] = v[1][gray_c(i)];
-    }
+    gray_walk<R>(gt, rg, [&](auto r, uint32_t g) {
+      constexpr int ri = decltype(r)::value;
+      psi_row[g] = v[0][ri];
+      if constexpr (ADJ) lam_row[g] = v[1][ri];
+    });
   }
 
   if (slot_cnt > 0) {
@@ -426,21 +514,19 @@ __global__ void __launch_bounds__(1 << (L - R)) pass_kernel(const PassArgs a) {
   }
 }
 
-}  // namespace qf
-
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
 
-namespace qf {
 template <int L, int R, bool ADJ>
 static int launch_pass(const PassArgs& a, const QfPass& hp, cudaStream_t stream) {
   constexpr int NT = 1 << (L - R);
   constexpr int NA = ADJ ? 2 : 1;
-  size_t smem = (size_t)NA * (1u << L) * sizeof(float2) +
-                (size_t)(hp.mat_end - hp.mat_begin) * sizeof(float2) +
-                (size_t)(hp.ang_end - hp.ang_begin) * 4 + (size_t)(hp.coef_end - hp.coef_begin) * 4 +
-                (size_t)(hp.slot_end - hp.slot_begin) * 8 + 16;
+  const size_t terms = (size_t)(hp.term_end - hp.term_begin);
+  size_t smem = (size_t)NA * (1u << L) * sizeof(float2) + (size_t)(hp.stage_end - hp.stage_begin) * sizeof(QfStage) +
+                (size_t)(hp.op_end - hp.op_begin) * sizeof(QfOp) + (size_t)(hp.slot_end - hp.slot_begin) * 8 +
+                (size_t)(hp.mat_end - hp.mat_begin) * sizeof(float2) + terms * 8 + (ADJ ? terms * 4 : 0) +
+                (size_t)(hp.grp_end - hp.grp_begin) * 4;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(pass_kernel<L, R, ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

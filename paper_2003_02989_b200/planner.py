@@ -30,11 +30,13 @@ from .circuit import generator_matrix, gate_matrix
 from .pauli import term_masks
 
 N_MIN = 10          # smaller registers are padded (extra qubits stay |0>)
-LANE_Q = 5          # qubits 0..4 are always lane bits at load/store
+LANE_Q = 4          # qubits 0..3 are always lane bits at load/store (128-byte runs)
 FWD_L, FWD_R = 13, 5
 ADJ_L, ADJ_R = 12, 4
 
 OP_DENSE1, OP_DENSE2, OP_DIAG, OP_OBS = 1, 2, 3, 4
+CLS_GENERAL, CLS_XLIKE, CLS_REAL = 0, 1, 2   # dense 1q matrix structure classes
+GK_MATRIX, GK_X, GK_Y, GK_Z = 0, 1, 2, 3     # adjoint generator kinds
 INIT_LOAD, INIT_ZERO, INIT_PRODUCT, INIT_LOAD_PSI = 0, 1, 2, 3
 
 STAGE_INTS, OP_INTS, PASS_INTS = 64, 16, 128
@@ -63,6 +65,7 @@ class GateInfo:
     gen: int = -1          # index in the generator table (symbolic gates)
     fixed: int = -1        # index in the fixed-matrix table (concrete dense gates)
     const_col: int = -1    # first constant-angle column (concrete diagonal gates)
+    cls: int = CLS_GENERAL  # dense 1q structure class (same for every row of a topology)
 
 
 def _is_z_only(terms) -> bool:
@@ -71,6 +74,30 @@ def _is_z_only(terms) -> bool:
 
 def _gate_terms(g):
     return [(dict(t.factors), float(t.coefficient)) for t in g.generator.terms]
+
+
+def _symbolic_class(terms, targets) -> int:
+    if len(targets) != 1:
+        return CLS_GENERAL
+    letters = {p for f, c in terms for p in f.values()}
+    has_ident = any(not f and c != 0.0 for f, c in terms)
+    if has_ident or len(letters) != 1:
+        return CLS_GENERAL
+    return {"X": CLS_XLIKE, "Y": CLS_REAL}.get(letters.pop(), CLS_GENERAL)
+
+
+def _matrix_class(m) -> int:
+    if m.shape[0] != 2:
+        return CLS_GENERAL
+    if np.all(m.imag == 0):
+        return CLS_REAL
+    if m[0, 0].imag == 0 and m[1, 1].imag == 0 and m[0, 1].real == 0 and m[1, 0].real == 0:
+        return CLS_XLIKE
+    return CLS_GENERAL
+
+
+def _concrete_class(g) -> int:
+    return _matrix_class(concrete_matrix(g))
 
 
 def topology_key(circuit, symbol_index) -> tuple:
@@ -82,7 +109,8 @@ def topology_key(circuit, symbol_index) -> tuple:
             gen = tuple(sorted((tuple(sorted(t.factors.items())), t.coefficient) for t in g.generator.terms))
             out.append(("s", tuple(g.targets), symbol_index[e.symbol], e.coeff, e.const, gen))
         else:
-            out.append(("c", tuple(g.targets), _concrete_is_diag(g)))
+            d = _concrete_is_diag(g)
+            out.append(("c", tuple(g.targets), d, CLS_GENERAL if d else _concrete_class(g)))
     return tuple(out)
 
 
@@ -110,9 +138,10 @@ def analyse(circuit, symbol_index) -> list[GateInfo]:
         if e is not None and e.symbol is not None:
             terms = _gate_terms(g)
             infos.append(GateInfo(i, tg, True, _is_z_only(terms), symbol_index[e.symbol],
-                                  float(e.coeff), float(e.const), terms))
+                                  float(e.coeff), float(e.const), terms, cls=_symbolic_class(terms, tg)))
         else:
-            infos.append(GateInfo(i, tg, False, _concrete_is_diag(g)))
+            d = _concrete_is_diag(g)
+            infos.append(GateInfo(i, tg, False, d, cls=CLS_GENERAL if d else _concrete_class(g)))
     return infos
 
 
@@ -433,11 +462,8 @@ def stage_slots(p: Pass, st: Stage, R: int):
     L = len(p.qubits)
     rs = set(st.regs)
     free = [b for b in range(L) if b not in rs]
-    lanes = [b for b in range(LANE_Q) if b not in rs]
-    if len(lanes) < LANE_Q:
-        lanes = free[:LANE_Q]
-    warps = [b for b in free if b not in lanes]
-    return list(st.regs), lanes + warps
+    # the 5 lowest free tile bits become lane bits (bits 0..LANE_Q-1 whenever free)
+    return list(st.regs), free
 
 
 # ---------------------------------------------------------------------------
@@ -648,6 +674,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         prow[8] = em.n_slots
         prow[11] = em.n_coef
         prow[13] = L
+        prow[14] = len(em.term_mask)
+        prow[80] = len(em.grp)
+        prow[82] = len(em.op_rows)
         outer = [q for q in range(n) if q not in set(p.qubits)]
         prow[10] = len(outer)
         prow[16:16 + len(outer)] = outer
@@ -682,6 +711,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         order = (a, b) if slot_of[a] < slot_of[b] else (b, a)
                         orow[1], orow[2] = slot_of[order[0]], slot_of[order[1]]
                     orow[3] = em.dense_mat(op, order)
+                    if op.kind == OP_DENSE1:
+                        cl = {infos[gi].cls for gi in op.factors}
+                        orow[9] = cl.pop() if len(cl) == 1 else CLS_GENERAL
                     if adjoint and op.symbolic:
                         (gi,) = op.factors
                         info = infos[gi]
@@ -689,6 +721,10 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         gm = gm * (2.0 * info.coeff)
                         orow[8] = len(em.genmats) // 2
                         em.genmats.extend(np.stack([gm.real, gm.imag], -1).reshape(-1).tolist())
+                        orow[10] = _generator_kind(info.terms) if op.kind == OP_DENSE1 else GK_MATRIX
+                        if orow[10] != GK_MATRIX:   # single Pauli: its scaled coefficient follows the matrix
+                            beta = sum(c for f, c in info.terms if f)
+                            em.genmats.extend([2.0 * info.coeff * beta, 0.0])
                         orow[7] = em.new_slot()
                         em.grad_slots.setdefault(info.sym, []).append(int(orow[7]))
                 elif op.kind == OP_DIAG:
@@ -704,7 +740,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                     for ti, t in enumerate(obs.terms):
                         xm, zm, ny = term_masks(t)
                         assert xm == 0
-                        terms.append((zm, em.n_coef, 0.0))
+                        terms.append((zm, -1 - em.n_coef, 0.0))  # negative: coefficient column
                         em.coef_cols.append((op.obs, ti))
                         em.n_coef += 1
                     b_, e_, g_ = em.emit_terms(terms, reg_glob)
@@ -722,6 +758,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         prow[7] = em.n_ang
         prow[9] = em.n_slots
         prow[12] = em.n_coef
+        prow[15] = len(em.term_mask)
+        prow[81] = len(em.grp)
+        prow[83] = len(em.op_rows)
         em.pass_rows.append(prow)
 
     # build recipe arrays
@@ -776,6 +815,13 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         recipe=recipe, grad_slots=em.grad_slots, obs_slots=em.obs_slots,
         energy_slots=em.energy_slots, stats=stats,
     )
+
+
+def _generator_kind(terms) -> int:
+    plain = [(f, c) for f, c in terms if f]
+    if len(plain) != 1 or len(plain[0][0]) != 1:
+        return GK_MATRIX
+    return {"X": GK_X, "Y": GK_Y, "Z": GK_Z}[next(iter(plain[0][0].values()))]
 
 
 _PAULI = {

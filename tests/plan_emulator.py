@@ -88,9 +88,9 @@ def check_invariants(prog: pl.Program):
         for si in range(sb, se):
             st = prog.stages[si]
             reg_glob = list(st[0:R])
-            lanes = list(st[8:13])
+            lanes = list(st[8:12])
             if si == sb or si == se - 1:
-                assert lanes == [0, 1, 2, 3, 4], (si, lanes)
+                assert lanes == [0, 1, 2, 3], (si, lanes)
             for o in prog.ops[st[48]:st[49]]:
                 if o[0] == pl.OP_DENSE2:
                     assert 0 <= o[1] < o[2] < R
@@ -135,7 +135,7 @@ def run_forward(prog: pl.Program, mats, angs, B, n, coefs=None, init_state=None)
                     elif o[0] == pl.OP_OBS:
                         h = np.zeros(dim)
                         for k in range(o[4], o[5]):
-                            h += coefs[prog.term_idx[k]] * _chi(idx, prog.term_mask[k])
+                            h += coefs[-1 - prog.term_idx[k]] * _chi(idx, prog.term_mask[k])
                         slots[b, o[7]] += float(np.sum(np.abs(psi[b]) ** 2 * h))
     return psi, slots
 
@@ -179,7 +179,7 @@ def run_adjoint(prog: pl.Program, mats, angs, B, n, psi, lam, hcoefs):
                     elif o[0] == pl.OP_OBS:
                         h = np.zeros(dim)
                         for k in range(o[4], o[5]):
-                            h += hcoefs[b, prog.term_idx[k]] * _chi(idx, prog.term_mask[k])
+                            h += hcoefs[b, -1 - prog.term_idx[k]] * _chi(idx, prog.term_mask[k])
                         lam[b] = h * psi[b]
                         slots[b, o[7]] += float(np.sum(np.abs(psi[b]) ** 2 * h))
     return slots
