@@ -148,8 +148,9 @@ class Bound:
     plan, concrete-gate tables, observable coefficient tables and reduction maps,
     all resident on the device.  ``execute`` then only launches kernels."""
 
-    def __init__(self, engine, circuits, symbol_names, observables, want_grad, device):
+    def __init__(self, engine, circuits, symbol_names, observables, want_grad, device, from_state=False):
         self.device = device
+        self.from_state = from_state
         self.symbol_names = list(symbol_names)
         sym_index = {s: i for i, s in enumerate(self.symbol_names)}
         self.circuits = list(circuits)
@@ -183,7 +184,7 @@ class Bound:
             self.hmix = torch.from_numpy(M).to(device)
             self.lam_diag = bool(self.hkeys) and all(all(p == "Z" for _, p in kk) for kk in self.hkeys)
         self.plan = engine.plan(template, sym_index, obs, want_grad, self.lam_diag,
-                                tuple(self.hkeys) if want_grad else None, device)
+                                tuple(self.hkeys) if want_grad else None, device, from_state)
         plan = self.plan
         fixed_np, const_np = pl.concrete_tables(self.circuits, plan.infos)
         self.fixed_rows, self.const_rows = fixed_np.shape[0], const_np.shape[0]
@@ -240,8 +241,9 @@ class Bound:
         return len(self.circuits)
 
     def execute(self, theta: torch.Tensor, *, upstream=None, want_state=False, want_grad=False,
-                want_expect=True, stream=None) -> dict:
-        """theta: device float32 [B, S].  Returns device tensors."""
+                want_expect=True, stream=None, initial=None) -> dict:
+        """theta: device float32 [B, S]; initial: [B, 2^n] complex state when bound
+        ``from_state`` (the circuit is applied to it instead of |0...0>).  Returns device tensors."""
         lib = nat.load()
         dev = self.device
         plan = self.plan
@@ -252,7 +254,19 @@ class Bound:
             theta = torch.zeros((B, 1), dtype=torch.float32, device=dev)
         fw = plan.fwd
         n_eff = plan.n_eff
-        psi = torch.empty((B, 1 << n_eff), dtype=torch.complex64, device=dev)
+        if self.from_state:
+            if initial is None:
+                raise ValueError("this binding applies the circuit to a given state: pass initial=")
+            init = torch.as_tensor(initial).to(device=dev, dtype=torch.complex64).reshape(B, -1)
+            if init.shape[1] != (1 << plan.n):
+                raise ValueError(f"initial state has {init.shape[1]} amplitudes, expected {1 << plan.n}")
+            if n_eff == plan.n:
+                psi = init.clone()  # kernels update psi in place; never alias the caller's tensor
+            else:
+                psi = torch.zeros((B, 1 << n_eff), dtype=torch.complex64, device=dev)
+                psi[:, : 1 << plan.n] = init
+        else:
+            psi = torch.empty((B, 1 << n_eff), dtype=torch.complex64, device=dev)
         mats = torch.empty((B, max(fw.prog.n_mat, 1)), dtype=torch.complex64, device=dev)
         angs = torch.empty((B, max(fw.prog.n_ang, 1)), dtype=torch.int32, device=dev)
         rec = fw.recipe(self.fixed_t, self.fixed_rows, self.const_t, self.const_rows)
@@ -336,9 +350,10 @@ class Engine:
         self._max_bound = max_bound
         self._lock = threading.Lock()
 
-    def plan(self, template, symbol_index, obs: ObsInfo, adjoint: bool, lam_diag: bool, hkeys, device):
+    def plan(self, template, symbol_index, obs: ObsInfo, adjoint: bool, lam_diag: bool, hkeys, device,
+             from_state: bool = False):
         topo = pl.topology_key(template, symbol_index)
-        key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device))
+        key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state)
         with self._lock:
             hit = self._plans.get(key)
         if hit is not None:
@@ -350,8 +365,9 @@ class Engine:
         for k in obs.diag_ids:
             diag_sums[k] = _TermList(obs.sums[k])
         fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
-                               obs_diag_ids=obs.diag_ids)
+                               obs_diag_ids=obs.diag_ids, from_state=from_state)
         plan = Plan(n, n_eff, len(symbol_index), infos, DeviceProgram(fwd, device), None, lam_diag, obs)
+        plan.extra["from_state"] = from_state
         if adjoint:
             infos_a = pl.analyse(template, symbol_index)
             hterms = _TermList([_Term(dict(kk), 1.0) for kk in hkeys])
@@ -363,16 +379,18 @@ class Engine:
             self._plans[key] = plan
         return plan
 
-    def bind(self, circuits, symbol_names, observables=(), *, want_grad=False, device=None) -> Bound:
+    def bind(self, circuits, symbol_names, observables=(), *, want_grad=False, device=None,
+             from_state=False) -> Bound:
         dev = _require_cuda(device)
         symbol_names = tuple(s.name if hasattr(s, "name") else s for s in symbol_names)
         observables = list(observables)
-        key = (tuple(map(id, circuits)), symbol_names, tuple(map(id, observables)), bool(want_grad), str(dev))
+        key = (tuple(map(id, circuits)), symbol_names, tuple(map(id, observables)), bool(want_grad), str(dev),
+               bool(from_state))
         with self._lock:
             hit = self._bound.get(key)
         if hit is not None and all(a is b for a, b in zip(hit.circuits, circuits)):
             return hit
-        b = Bound(self, circuits, symbol_names, observables, want_grad, dev)
+        b = Bound(self, circuits, symbol_names, observables, want_grad, dev, from_state)
         b._keepalive = observables
         with self._lock:
             if len(self._bound) >= self._max_bound:

@@ -1,0 +1,387 @@
+"""Differentiators on the GPU engine, behind the reference's gradient API (qcflow/gradients.py).
+
+* ``adjoint_grad`` / ``Adjoint`` -- new: one forward + one backward sweep
+  (tile-pass ADJ kernels).  The reference lists adjoint differentiation as a
+  non-goal; its oracle is the exact parameter-shift gradient.
+* ``parameter_shift_grad`` / ``ParameterShift`` -- the reference's exact PS rule
+  (gradients.py:158-165, driver :241-326): every symbolic gate is rewritten as a
+  product of per-term exponentials and each term angle is shifted by +-pi/4.  Here all
+  ``2*sum_occ K`` shifted circuits share one topology (each term angle is its own
+  pseudo-parameter column), so the whole PS gradient is ONE batched execution.
+* ``finite_difference_grad`` -- gradients.py:113-155, shifted points as batch rows.
+* ``stochastic_ps_grad`` -- gradients.py:168-174 with the reference's sampling axes,
+  evaluated through :class:`GpuEvaluator` (the evaluator protocol, :96-110).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Mapping
+
+import numpy as np
+import torch
+
+from .circuit import Circuit, Gate, ParamExpr, circuit_symbols, normalize_bindings
+from .pauli import PauliString, PauliSum, all_terms_commute, as_pauli_sum
+from .sampling import derive_seed
+
+CENTRAL = "central"
+FORWARD = "forward"
+SHIFT = math.pi / 4.0
+
+
+@dataclass(frozen=True)
+class Exact:
+    """Exact expectation values."""
+
+
+@dataclass(frozen=True)
+class Sampled:
+    shots: int
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.shots < 1:
+            raise ValueError("shots must be >= 1")
+        if self.seed < 0:
+            raise ValueError("seed must be non-negative")
+
+
+@dataclass(frozen=True)
+class GradRequest:
+    circuit: Circuit
+    observable: object
+    bindings: Mapping
+    estimator: object = Exact()
+
+
+@dataclass
+class GradResult:
+    gradient: np.ndarray
+    evaluations: int
+    degenerate_sampling: bool = False
+
+
+@dataclass(frozen=True)
+class StochasticConfig:
+    sample_generator_terms: bool = False
+    sample_cost_terms: bool = False
+    sample_coordinates: bool = False
+    num_samples: int = 1
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.num_samples < 1:
+            raise ValueError("num_samples must be >= 1")
+        if self.seed < 0:
+            raise ValueError("seed must be non-negative")
+
+
+def _is_sampled(est) -> bool:
+    return type(est).__name__ == "Sampled" and hasattr(est, "shots")
+
+
+class GpuEvaluator:
+    """Evaluator protocol (ref gradients.py:96-110): ``ev(resolved_circuit, observable, key=None)``."""
+
+    def __init__(self, estimator=Exact()):
+        self.estimator = estimator
+        self.count = 0
+
+    def __call__(self, circuit, observable, key: tuple = None) -> float:
+        from . import sim
+
+        if key is None:
+            key = (self.count,)
+        self.count += 1
+        if _is_sampled(self.estimator):
+            seed = derive_seed(self.estimator.seed, *key)
+            return sim.sampled_expectation(circuit, observable, self.estimator.shots, seed)
+        return sim.expectation(sim.simulate(circuit), observable)
+
+
+def _require(symbols, bindings):
+    miss = [s for s in symbols if s not in bindings]
+    if miss:
+        raise KeyError(f"missing binding for symbol(s): {', '.join(miss)}")
+
+
+def _finite(g):
+    if not np.all(np.isfinite(g)):
+        raise ValueError("gradient has non-finite entries")
+
+
+# ---------------------------------------------------------------------------
+# adjoint
+# ---------------------------------------------------------------------------
+
+
+def adjoint_grad(req: GradRequest) -> GradResult:
+    """Exact gradient by the adjoint method (one forward + one backward sweep)."""
+    if _is_sampled(req.estimator):
+        raise ValueError("the adjoint differentiator needs the Exact estimator")
+    c = req.circuit
+    obs = as_pauli_sum(req.observable)
+    b = normalize_bindings(req.bindings)
+    syms = circuit_symbols(c)
+    _require(syms, b)
+    if not syms:
+        return GradResult(np.zeros(0), 0)
+    from .ops import expectation_and_gradient
+
+    _, g = expectation_and_gradient([c], syms, np.array([[b[s] for s in syms]], dtype=np.float32), [obs])
+    g = np.asarray(g[0], dtype=np.float64)
+    _finite(g)
+    return GradResult(g, 1)
+
+
+class Adjoint:
+    """Adjoint differentiator engine (``engine(GradRequest) -> GradResult``)."""
+
+    def __call__(self, request: GradRequest) -> GradResult:
+        return adjoint_grad(request)
+
+
+# ---------------------------------------------------------------------------
+# parameter shift, batched on the GPU
+# ---------------------------------------------------------------------------
+
+
+def _ps_expand(circuit, bindings, symbols):
+    """Per-term rewrite used by PS (ref gradients.py:224-238): symbolic gate j with
+    non-identity terms beta_k P_k becomes gates exp(-i eta_jk P_k) with pseudo-symbol
+    eta_jk = (coeff_j * theta + const_j) * beta_k.  Returns (circuit, names, values, occ)."""
+    index = {s: i for i, s in enumerate(symbols)}
+    gates, names, vals, occ = [], [], [], []
+    for j, g in enumerate(circuit.gates):
+        e = g.exponent
+        if e is None or e.symbol is None:
+            gates.append(g)
+            continue
+        gen = as_pauli_sum(g.generator)
+        if not all_terms_commute(gen):
+            raise ValueError(f"gate {j}: generator terms do not commute, so the parameter-shift "
+                             "rule does not apply — use finite_difference_grad instead")
+        v = e.coeff * float(bindings[e.symbol]) + e.const
+        for t in gen.terms:
+            if not t.factors or t.coefficient == 0.0:
+                continue  # identity terms: global phase only
+            name = f"__ps{j}_{len(names)}"
+            gates.append(Gate(tuple(sorted(t.factors)), exponent=ParamExpr(name),
+                              generator=PauliSum([PauliString(1.0, t.factors)])))
+            names.append(name)
+            vals.append(v * t.coefficient)
+            occ.append((index[e.symbol], e.coeff * t.coefficient))
+    return Circuit(circuit.num_qubits, gates), names, np.array(vals, dtype=np.float64), occ
+
+
+def _ps_rows(base, k_count):
+    rows = np.repeat(base[None, :], 2 * k_count, axis=0)
+    for k in range(k_count):
+        rows[2 * k, k] += SHIFT
+        rows[2 * k + 1, k] -= SHIFT
+    return rows
+
+
+def _batched_expect(circuit, names, rows, obs, chunk_amps=1 << 31):
+    from .ops import expectation
+
+    n = circuit.num_qubits
+    per = max(1, chunk_amps >> max(n, 10))
+    out = np.empty(rows.shape[0])
+    for s in range(0, rows.shape[0], per):
+        out[s:s + per] = expectation(circuit, names, rows[s:s + per].astype(np.float32), [obs])[:, 0]
+    return out
+
+
+def parameter_shift_grad(req: GradRequest, evaluator=None) -> GradResult:
+    """Exact PS gradient (ref gradients.py:158-165): 2 evaluations per (occurrence, term),
+    all executed as one batched GPU launch sequence when no custom evaluator is given."""
+    if evaluator is not None or _is_sampled(req.estimator):
+        return stochastic_ps_grad(req, StochasticConfig(), evaluator)
+    c = req.circuit
+    obs = as_pauli_sum(req.observable)
+    b = normalize_bindings(req.bindings)
+    syms = circuit_symbols(c)
+    _require(syms, b)
+    if not syms:
+        return GradResult(np.zeros(0), 0)
+    ec, names, base, occ = _ps_expand(c, b, syms)
+    if not names:
+        return GradResult(np.zeros(len(syms)), 0)
+    f = _batched_expect(ec, names, _ps_rows(base, len(names)), obs)
+    grad = np.zeros(len(syms))
+    for k, (si, w) in enumerate(occ):
+        grad[si] += w * (f[2 * k] - f[2 * k + 1])
+    _finite(grad)
+    return GradResult(grad, 2 * len(names))
+
+
+class ParameterShift:
+    """Exact parameter-shift engine, GPU-batched (ref graph.py:54-58)."""
+
+    def __call__(self, request: GradRequest) -> GradResult:
+        return parameter_shift_grad(request)
+
+
+def finite_difference_grad(req: GradRequest, scheme: str = CENTRAL, epsilon: float = 1e-4,
+                           evaluator=None) -> GradResult:
+    """ref gradients.py:113-155; shifted points are batch rows of one execution.
+    (In complex64 the central stencil needs epsilon >~ 1e-3 to beat rounding.)"""
+    if scheme not in (CENTRAL, FORWARD):
+        raise ValueError(f"unknown scheme {scheme!r} (want {CENTRAL!r} or {FORWARD!r})")
+    if not epsilon > 0:
+        raise ValueError("epsilon must be positive")
+    c = req.circuit
+    obs = as_pauli_sum(req.observable)
+    b = normalize_bindings(req.bindings)
+    syms = circuit_symbols(c)
+    _require(syms, b)
+    if not syms:
+        return GradResult(np.zeros(0), 0)
+    base = np.array([b[s] for s in syms], dtype=np.float64)
+    S = len(syms)
+    if evaluator is not None or _is_sampled(req.estimator):
+        ev = GpuEvaluator(req.estimator) if evaluator is None else evaluator
+        start = ev.count
+        from .circuit import resolve
+
+        def f(point):
+            return ev(resolve(c, dict(zip(syms, point))), obs)
+
+        g = np.zeros(S)
+        if scheme == CENTRAL:
+            for k in range(S):
+                e = np.zeros(S); e[k] = epsilon
+                g[k] = (f(base + e) - f(base - e)) / (2 * epsilon)
+        else:
+            f0 = f(base)
+            for k in range(S):
+                e = np.zeros(S); e[k] = epsilon
+                g[k] = (f(base + e) - f0) / epsilon
+        _finite(g)
+        return GradResult(g, ev.count - start)
+    eye = np.eye(S) * epsilon
+    if scheme == CENTRAL:
+        rows = np.concatenate([base + eye, base - eye])
+        vals = _batched_expect(c, syms, rows, obs)
+        g = (vals[:S] - vals[S:]) / (2 * epsilon)
+        n_eval = 2 * S
+    else:
+        rows = np.concatenate([base[None], base + eye])
+        vals = _batched_expect(c, syms, rows, obs)
+        g = (vals[1:] - vals[0]) / epsilon
+        n_eval = S + 1
+    _finite(g)
+    return GradResult(g, n_eval)
+
+
+class FiniteDifference:
+    def __init__(self, scheme: str = CENTRAL, epsilon: float = 1e-3):
+        if epsilon <= 0:
+            raise ValueError("epsilon must be positive")
+        self.scheme = scheme
+        self.epsilon = float(epsilon)
+
+    def __call__(self, request: GradRequest) -> GradResult:
+        return finite_difference_grad(request, self.scheme, self.epsilon)
+
+
+# ---------------------------------------------------------------------------
+# stochastic parameter shift (reference sampling axes, GPU evaluator)
+# ---------------------------------------------------------------------------
+
+
+def stochastic_ps_grad(req: GradRequest, cfg: StochasticConfig, evaluator=None) -> GradResult:
+    """ref gradients.py:168-174 / :241-326: Monte-Carlo PS over generator terms, cost terms
+    and coordinates with importance weights; substreams keyed exactly as the reference."""
+    from .sampling import philox_key  # noqa: F401  (keeps the RNG module loaded)
+
+    c = req.circuit
+    obs = as_pauli_sum(req.observable)
+    b = normalize_bindings(req.bindings)
+    syms = circuit_symbols(c)
+    _require(syms, b)
+    if not syms:
+        return GradResult(np.zeros(0), 0)
+    index = {s: i for i, s in enumerate(syms)}
+    occs = []
+    for j, g in enumerate(c.gates):
+        e = g.exponent
+        if e is None or e.symbol is None:
+            continue
+        gen = as_pauli_sum(g.generator)
+        if not all_terms_commute(gen):
+            raise ValueError(f"gate {j}: generator terms do not commute, so the parameter-shift "
+                             "rule does not apply — use finite_difference_grad instead")
+        terms = tuple(t for t in gen.terms if t.factors and t.coefficient != 0.0)
+        occs.append((j, index[e.symbol], e.coeff, e.coeff * b[e.symbol] + e.const, terms))
+    base = [g.resolved(b) for g in c.gates]
+    ev = GpuEvaluator(req.estimator) if evaluator is None else evaluator
+    start = ev.count
+    cost = [t for t in obs.terms if t.factors and t.coefficient != 0.0]
+    cmass = np.array([abs(t.coefficient) for t in cost])
+    ctot = float(cmass.sum())
+    omass = np.array([abs(o[2]) * sum(abs(t.coefficient) for t in o[4]) for o in occs])
+    otot = float(omass.sum())
+    degenerate = False
+    acc = np.zeros(len(syms))
+
+    def shifted(occ, k, delta):
+        j, _, _, v, terms = occ
+        exp = [Gate(t.support, exponent=ParamExpr(None, 0.0, v * t.coefficient + (delta if kk == k else 0.0)),
+                    generator=PauliSum([t.with_coefficient(1.0)])) for kk, t in enumerate(terms)]
+        return Circuit(c.num_qubits, base[:j] + exp + base[j + 1:])
+
+    for i in range(cfg.num_samples):
+        rng = np.random.Generator(np.random.Philox(np.random.SeedSequence(cfg.seed, spawn_key=(i,))))
+        counter = 0
+        smp = np.zeros(len(syms))
+        if cfg.sample_coordinates:
+            if otot == 0.0:
+                degenerate, chosen = True, []
+            else:
+                pr = omass / otot
+                pick = int(rng.choice(len(occs), p=pr))
+                chosen = [(occs[pick], 1.0 / pr[pick])]
+        else:
+            chosen = [(o, 1.0) for o in occs]
+        for occ, cw in chosen:
+            terms = occ[4]
+            btot = sum(abs(t.coefficient) for t in terms)
+            if cfg.sample_generator_terms:
+                if btot == 0.0:
+                    degenerate = True
+                    continue
+                k = int(rng.choice(len(terms), p=np.array([abs(t.coefficient) for t in terms]) / btot))
+                pairs = [(k, occ[2] * math.copysign(1.0, terms[k].coefficient) * btot)]
+            else:
+                pairs = [(k, occ[2] * t.coefficient) for k, t in enumerate(terms)]
+            for k, w in pairs:
+                if w == 0.0:
+                    continue
+                if cfg.sample_cost_terms:
+                    if ctot == 0.0:
+                        degenerate = True
+                        continue
+                    m = int(rng.choice(len(cost), p=cmass / ctot))
+                    o_eff = PauliSum([cost[m].with_coefficient(math.copysign(1.0, cost[m].coefficient) * ctot)])
+                else:
+                    o_eff = obs
+                fp = ev(shifted(occ, k, +SHIFT), o_eff, key=(i, 0, counter))
+                fm = ev(shifted(occ, k, -SHIFT), o_eff, key=(i, 1, counter))
+                counter += 1
+                smp[occ[1]] += cw * w * (fp - fm)
+        acc += smp
+    g = acc / cfg.num_samples
+    _finite(g)
+    return GradResult(g, ev.count - start, degenerate)
+
+
+class StochasticShift:
+    def __init__(self, config: StochasticConfig):
+        self.config = config
+
+    def __call__(self, request: GradRequest) -> GradResult:
+        return stochastic_ps_grad(request, self.config)

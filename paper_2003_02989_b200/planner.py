@@ -617,14 +617,19 @@ def _walsh_angles(diag_entries: np.ndarray) -> np.ndarray:
 
 
 def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool,
-                  observables=None, obs_diag_ids=(), lam_diag: bool = False) -> Program:
+                  observables=None, obs_diag_ids=(), lam_diag: bool = False,
+                  from_state: bool = False) -> Program:
     """Plan + emit.  ``observables``: list of PauliSums; ``obs_diag_ids``: those fused as
     OBS ops at the end of the forward program; ``lam_diag``: adjoint with a diagonal H
-    whose lambda-init / energy is fused into the first backward pass."""
+    whose lambda-init / energy is fused into the first backward pass; ``from_state``:
+    the forward program starts from a caller-provided state instead of |0...0>."""
     L, R = (ADJ_L, ADJ_R) if adjoint else (FWD_L, FWD_R)
     L = min(L, n)
     ops = build_ops(infos, adjoint)
-    ops, init = absorb_product_init(ops, infos, n, allow_symbolic=not adjoint)
+    if from_state and not adjoint:
+        init = {}
+    else:
+        ops, init = absorb_product_init(ops, infos, n, allow_symbolic=not adjoint)
     # observable ops
     obs_ops = []
     if not adjoint:
@@ -667,7 +672,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
             prow[2] = (INIT_LOAD_PSI if lam_diag else INIT_LOAD) if last_fwd else INIT_LOAD
             prow[3] = 0 if first_fwd else 1
         else:
-            prow[2] = (INIT_PRODUCT if init else INIT_ZERO) if first_fwd else INIT_LOAD
+            prow[2] = INIT_LOAD if (from_state or not first_fwd) else (INIT_PRODUCT if init else INIT_ZERO)
             prow[3] = 1
         prow[4] = em.n_mat
         prow[6] = em.n_ang

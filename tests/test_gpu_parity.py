@@ -1,0 +1,314 @@
+"""GPU parity tests: the CUDA path (through the drop-in API / C ABI) vs the CPU oracle
+and the reference's golden vectors.
+
+Tolerances (BASELINE.json north star, complex64 arithmetic):
+  * amplitudes             1e-5 absolute
+  * expectations           1e-4 absolute
+  * gradients              1e-4 absolute + 1e-5 relative.  The relative part only matters for
+                           gradients above ~10 in magnitude: complex64 itself cannot do better
+                           there (the same adjoint restated in NumPy complex64 is off by 1.7e-4 on
+                           the 16-qubit QAOA family with |g| ~ 23).
+  * sampled bitstrings     bit-exact for identical states and seeds.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from circuits import random_circuit, random_observable
+from oracle import qcflow_port as orc
+from paper_2003_02989_b200 import gates as G
+from paper_2003_02989_b200 import gradients as gr
+from paper_2003_02989_b200 import ops, sim
+from paper_2003_02989_b200 import workloads as wl
+from paper_2003_02989_b200.circuit import Circuit, ParamExpr, Symbol, circuit_symbols, from_json, resolve
+from paper_2003_02989_b200.pauli import PauliString, PauliSum, identity, pauli_sum_from_obj, pauli_x, pauli_z
+
+pytestmark = pytest.mark.gpu
+
+AMP, EXP, GABS, GREL = 1e-5, 1e-4, 1e-4, 1e-5
+
+
+def _obs(s):
+    return pauli_sum_from_obj(json.loads(s))
+
+
+def _close_grad(got, want):
+    np.testing.assert_allclose(got, want, atol=GABS, rtol=GREL)
+
+
+# ---------------------------------------------------------------------------
+# golden vectors from the reference
+# ---------------------------------------------------------------------------
+
+
+def test_known_answers(cuda, golden):
+    meta, arr = golden
+    bell = from_json(meta["cases"]["bell"]["circuit"])
+    s = sim.simulate(bell)
+    np.testing.assert_allclose(s.amplitudes, arr["bell/amps"], atol=AMP)
+    assert sim.expectation(s, PauliString(1.0, {0: "Z", 1: "Z"})) == pytest.approx(1.0, abs=EXP)
+    assert sim.expectation(s, pauli_z(0)) == pytest.approx(0.0, abs=EXP)
+    c = Circuit(1, [G.xpow(Symbol("theta"), 0)])
+    out = sim.batch_execute([c, c, c], [[0.0], [1.0], [2.0]], [pauli_z(0)])
+    np.testing.assert_allclose(out, [[1.0], [-1.0], [1.0]], atol=EXP)
+    # little endian: X on qubit q sets bit q
+    for q in range(6):
+        st = sim.simulate(Circuit(6, [G.x(q)]))
+        np.testing.assert_allclose(st.amplitudes, np.eye(64)[1 << q], atol=AMP)
+        assert sim.expectation(st, pauli_z(q)) == pytest.approx(-1.0, abs=EXP)
+
+
+@pytest.mark.parametrize("i", range(8))
+def test_golden_states_and_expectations(cuda, golden, i):
+    meta, arr = golden
+    case = meta["cases"][f"concrete{i}"]
+    c = from_json(case["circuit"])
+    st = sim.simulate(c)
+    np.testing.assert_allclose(st.amplitudes, arr[f"concrete{i}/amps"], atol=AMP)
+    for o, e in zip(case["observables"], case["expectations"]):
+        assert sim.expectation(st, _obs(o)) == pytest.approx(e, abs=EXP)
+
+
+@pytest.mark.parametrize("i", range(4))
+def test_golden_gradients_adjoint_and_ps(cuda, golden, i):
+    meta, arr = golden
+    case = meta["cases"][f"symbolic{i}"]
+    c = from_json(case["circuit"])
+    o = _obs(case["observable"])
+    b = dict(zip(case["symbols"], case["bindings"]))
+    req = gr.GradRequest(c, o, b)
+    _close_grad(gr.adjoint_grad(req).gradient, arr[f"symbolic{i}/ps"])
+    ps = gr.parameter_shift_grad(req)
+    _close_grad(ps.gradient, arr[f"symbolic{i}/ps"])
+    assert ps.evaluations == case["ps_evaluations"]
+
+
+def test_golden_config_families(cuda, golden):
+    meta, arr = golden
+    cfg = meta["configs"]
+    for name in ("hea", "qaoa"):
+        c = from_json(cfg[name]["circuit"])
+        o = _obs(cfg[name]["observable"])
+        rows = np.array(cfg[name]["rows"], dtype=np.float32)
+        e, g = ops.expectation_and_gradient(c, circuit_symbols(c), rows, [o])
+        np.testing.assert_allclose(e, arr[f"{name}/exp"], atol=EXP)
+        _close_grad(g, arr[f"{name}/ps"])
+    c = from_json(cfg["qcnn"]["circuit"])
+    o = _obs(cfg["qcnn"]["observable"])
+    e, g = ops.expectation_and_gradient(c, circuit_symbols(c), np.array([cfg["qcnn"]["row"]], dtype=np.float32), [o])
+    np.testing.assert_allclose(e[0], arr["qcnn/exp"][0], atol=EXP)
+    _close_grad(g[0], arr["qcnn/ps"])
+    c = from_json(cfg["rcs"]["circuit"])
+    np.testing.assert_allclose(sim.simulate(c).amplitudes, arr["rcs/amps"], atol=AMP)
+    c = from_json(cfg["big"]["circuit"])
+    assert sim.expectation(sim.simulate(c), _obs(cfg["big"]["observable"])) == pytest.approx(
+        cfg["big"]["expectation"], abs=EXP)
+
+
+# ---------------------------------------------------------------------------
+# CUDA path vs oracle on seeded random inputs
+# ---------------------------------------------------------------------------
+
+
+@pytest.mark.parametrize("seed,n", [(0, 3), (1, 9), (2, 10), (3, 12), (4, 13), (5, 14), (6, 16), (7, 17)])
+def test_states_expectations_gradients_vs_oracle(cuda, seed, n):
+    rng = np.random.default_rng(100 + seed)
+    c = random_circuit(rng, n, 150, n_sym=5)
+    syms = circuit_symbols(c)
+    theta = rng.uniform(-3, 3, size=(3, len(syms))).astype(np.float32)
+    obs = [random_observable(rng, n, diag=True), random_observable(rng, n, diag=False)]
+    states = ops.state([c] * 3, syms, theta)
+    e, g = ops.expectation_and_gradient([c] * 3, syms, theta, obs, upstream=np.array([[1.0, 0.5]] * 3))
+    for b in range(3):
+        bind = dict(zip(syms, theta[b].astype(np.float64)))
+        ref = orc.simulate_amps(c, bind)
+        np.testing.assert_allclose(states[b], ref, atol=AMP)
+        for k, o in enumerate(obs):
+            assert e[b, k] == pytest.approx(orc.expectation(ref, o, n), abs=EXP)
+        weighted = obs[0] + obs[1] * 0.5
+        _close_grad(g[b], orc.adjoint_grad(c, weighted, bind)[1])
+
+
+def test_batch_rows_with_different_concrete_values(cuda):
+    """QCNN-style data circuits: same topology, per-row concrete angles (ref graph.py:443-468)."""
+    rng = np.random.default_rng(7)
+    model = wl.qcnn_model(8)
+    rows = []
+    for _ in range(5):
+        data = wl.qcnn_data_circuit(rng.uniform(-np.pi, np.pi, 8))
+        rows.append(Circuit(8, tuple(data.gates) + tuple(model.gates)))
+    syms = circuit_symbols(model)
+    theta = rng.uniform(0, 2, size=(5, len(syms))).astype(np.float32)
+    z7 = PauliSum([PauliString(1.0, {7: "Z"})])
+    e, g = ops.expectation_and_gradient(rows, syms, theta, [z7])
+    for b in range(5):
+        bind = dict(zip(syms, theta[b].astype(np.float64)))
+        ee, gg = orc.adjoint_grad(rows[b], z7, bind)
+        assert e[b, 0] == pytest.approx(ee, abs=EXP)
+        _close_grad(g[b], gg)
+
+
+def test_sampler_bit_exact_on_identical_states(cuda):
+    import torch
+
+    from paper_2003_02989_b200.sampling import philox_key, sample_indices
+
+    rng = np.random.default_rng(11)
+    for n in (10, 13, 16):
+        c = random_circuit(rng, n, 80)
+        psi = ops.state([c] * 3, [], np.zeros((3, 0), dtype=np.float32))
+        seeds = [3, 99, 123456]
+        idx, near = sample_indices(psi.contiguous(), n, 700, [philox_key(s) for s in seeds])
+        st = psi.cpu().numpy().astype(np.complex128)
+        for b in range(3):
+            want = orc.draw_indices(st[b], n, 700, orc.substream(seeds[b]))
+            np.testing.assert_array_equal(idx[b].cpu().numpy(), want)
+        assert int(near.sum()) == 0
+
+
+def test_sample_api_matches_oracle_draw_on_gpu_state(cuda):
+    rng = np.random.default_rng(12)
+    c = random_circuit(rng, 7, 40)
+    st = sim.simulate(c)
+    got = sim.sample(st, 500, seed=17).bitstrings
+    want = orc.sample(st.device_amplitudes().cpu().numpy().astype(np.complex128), 7, 500, 17)
+    np.testing.assert_array_equal(got, want)
+    with pytest.raises(ValueError):
+        sim.sample(st, 0, seed=1)
+
+
+def test_sampled_expectation_bit_exact_semantics(cuda):
+    """Same draw semantics as ref sim.py:245-272: feed the oracle the GPU's rotated states."""
+    rng = np.random.default_rng(13)
+    c = random_circuit(rng, 5, 30)
+    obs = PauliSum([PauliString(0.8, {0: "X", 2: "Z"}), PauliString(-0.5, {1: "Y"}), identity(0.25),
+                    PauliString(0.3, {3: "Z", 4: "Z"})])
+    got = sim.sampled_expectation(c, obs, 600, seed=101)
+    rotated = {}
+    for k, t in enumerate(obs.terms):
+        if t.factors:
+            rc = Circuit(5, tuple(c.gates) + tuple(sim.basis_change_gates(t)))
+            rotated[k] = sim.simulate(rc).device_amplitudes().cpu().numpy().astype(np.complex128)
+    want = orc.sampled_expectation(c, obs, 600, 101, rotated_states=rotated)
+    assert got == pytest.approx(want, abs=1e-12)
+    # exact cases (ref test_sim.py:284-306)
+    bell = Circuit(2, [G.h(0), G.cnot(0, 1)])
+    assert sim.sampled_expectation(bell, PauliString(1.0, {0: "Z", 1: "Z"}), 2000, seed=11) == 1.0
+    assert sim.sampled_expectation(Circuit(1, [G.h(0)]), pauli_x(0), 2000, seed=13) == 1.0
+    assert sim.sampled_expectation(Circuit(1, [G.h(0), G.s(0)]), PauliString(1.0, {0: "Y"}), 500, seed=17) == 1.0
+    assert sim.sampled_expectation(Circuit(1, []), PauliSum([identity(2.5), pauli_z(0)]), 1, seed=0) == 3.5
+
+
+def test_run_ops_apply_matrix_unitary(cuda):
+    rng = np.random.default_rng(14)
+    from circuits import random_unitary
+
+    n = 5
+    amps = rng.normal(size=(4, 2 ** n)) + 1j * rng.normal(size=(4, 2 ** n))
+    amps /= np.linalg.norm(amps, axis=1, keepdims=True)
+    for tg in [(0,), (2,), (4,), (1, 3), (3, 1), (0, 4), (4, 2)]:
+        u = random_unitary(2 ** len(tg), rng)
+        np.testing.assert_allclose(sim.apply_matrix(amps, u, tg, n), orc.apply_matrix(amps, u, tg, n), atol=AMP)
+    c = random_circuit(rng, 3, 12)
+    np.testing.assert_allclose(sim.unitary(c)[:, 0], sim.simulate(c).amplitudes, atol=AMP)
+
+
+def test_parameter_shift_gpu_matches_oracle_ps(cuda):
+    rng = np.random.default_rng(15)
+    c = random_circuit(rng, 6, 40, n_sym=4)
+    o = random_observable(rng, 6)
+    b = {s: float(rng.uniform(-2, 2)) for s in circuit_symbols(c)}
+    want, n_eval = orc.parameter_shift_grad(c, o, b)
+    res = gr.parameter_shift_grad(gr.GradRequest(c, o, b))
+    _close_grad(res.gradient, want)
+    assert res.evaluations == n_eval
+    fd = gr.finite_difference_grad(gr.GradRequest(c, o, b), epsilon=2e-3)
+    np.testing.assert_allclose(fd.gradient, want, atol=5e-3)
+
+
+# ---------------------------------------------------------------------------
+# edge cases and error behaviour (reference exception classes)
+# ---------------------------------------------------------------------------
+
+
+def test_edge_cases(cuda, monkeypatch):
+    st = sim.simulate(Circuit(3))
+    np.testing.assert_allclose(st.amplitudes, np.eye(8)[0], atol=AMP)
+    assert sim.expectation(sim.StateVector.zero(1), identity(2.5)) == 2.5
+    with pytest.raises(KeyError, match="t"):
+        sim.simulate(Circuit(1, [G.rx("t", 0)]))
+    monkeypatch.setenv("QCFLOW_MAX_QUBITS", "3")
+    with pytest.raises(MemoryError, match="QCFLOW_MAX_QUBITS"):
+        sim.simulate(Circuit(4, [G.h(0)]))
+    monkeypatch.setenv("QCFLOW_MAX_QUBITS", "junk")
+    with pytest.raises(ValueError, match="junk"):
+        sim.simulate(Circuit(4, [G.h(0)]))
+    monkeypatch.delenv("QCFLOW_MAX_QUBITS")
+    c = Circuit(2, [G.rx("a", 0), G.ry("b", 1)])
+    with pytest.raises(ValueError, match="ragged"):
+        sim.batch_execute([c], [[0.1]], [pauli_z(0)])
+    assert sim.batch_execute([], [], [pauli_z(0)]).shape == (0, 1)
+    with pytest.raises(ValueError, match="commute"):
+        bad = Circuit(1, [G.Gate((0,), exponent=ParamExpr("s"), generator=PauliSum([pauli_x(0), pauli_z(0)]))])
+        gr.parameter_shift_grad(gr.GradRequest(bad, pauli_z(0), {"s": 0.3}))
+    with pytest.raises(KeyError):
+        gr.adjoint_grad(gr.GradRequest(c, pauli_z(0), {"a": 0.1}))
+    # zero upstream -> zero gradient; identity-only generator contributes zero
+    _, g = ops.expectation_and_gradient(c, ["a", "b"], np.array([[0.3, 0.4]], np.float32), [pauli_z(0)],
+                                        upstream=np.zeros((1, 1)))
+    np.testing.assert_allclose(g, 0.0, atol=1e-12)
+
+
+def test_batch_permutation_invariance_and_upstream_linearity(cuda):
+    circ, cost = wl.qaoa_circuit(12, 2, wl.qaoa_graph(12, seed=5))
+    syms = circuit_symbols(circ)
+    th = wl.qaoa_params(6, 2)
+    perm = np.array([3, 0, 5, 1, 4, 2])
+    e1, g1 = ops.expectation_and_gradient(circ, syms, th, [cost])
+    e2, g2 = ops.expectation_and_gradient(circ, syms, th[perm], [cost])
+    np.testing.assert_allclose(e2, e1[perm], atol=1e-12)
+    np.testing.assert_allclose(g2, g1[perm], atol=1e-12)
+    _, g3 = ops.expectation_and_gradient(circ, syms, th, [cost], upstream=np.full((6, 1), 2.5))
+    np.testing.assert_allclose(g3, 2.5 * g1, rtol=1e-5, atol=1e-5)
+
+
+# ---------------------------------------------------------------------------
+# full-size properties (BASELINE configs) -- size-independent checks
+# ---------------------------------------------------------------------------
+
+
+def test_qaoa20_full_batch_properties(cuda):
+    import torch
+
+    circ, cost = wl.qaoa_circuit(20, 4, wl.qaoa_graph(20))
+    syms = circuit_symbols(circ)
+    th = torch.as_tensor(wl.qaoa_params(256, 4)).cuda()
+    st = ops.state(circ, syms, th[:8])
+    norms = (st.abs() ** 2).sum(dim=1).double().cpu().numpy()
+    np.testing.assert_allclose(norms, 1.0, atol=1e-5)
+    e, g = ops.expectation_and_gradient(circ, syms, th, [cost])
+    assert e.shape == (256, 1) and g.shape == (256, 8)
+    # spot-check two rows against the oracle's adjoint restatement
+    for b in (0, 255):
+        bind = dict(zip(syms, th[b].double().cpu().numpy()))
+        ee, gg = orc.adjoint_grad(circ, cost, bind)
+        assert float(e[b, 0]) == pytest.approx(ee, abs=EXP)
+        _close_grad(g[b].cpu().numpy(), gg)
+
+
+def test_rcs24_sampling_bit_exact(cuda):
+    """Config 4 circuits at full size: 24 qubits, depth 20; bitstrings identical to the
+    reference draw on the same (upcast) state and seed."""
+    circs = wl.rcs_circuits(2, 24, 20)
+    from paper_2003_02989_b200.sampling import derive_seed
+
+    seeds = [derive_seed(wl.SEED_RCS_SHOTS, b) for b in range(2)]
+    bits = ops.sample(circs, [], np.zeros((2, 0), np.float32), 1000, seed=seeds)
+    st = ops.state(circs, [], np.zeros((2, 0), np.float32))
+    for b in range(2):
+        want = orc.sample(st[b].astype(np.complex128), 24, 1000, seeds[b])
+        np.testing.assert_array_equal(bits[b], want)
+    norms = (np.abs(st) ** 2).sum(axis=1)
+    np.testing.assert_allclose(norms, 1.0, atol=1e-5)

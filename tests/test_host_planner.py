@@ -1,0 +1,121 @@
+"""Host-side logic on the CPU: IR mirror, recipes, and the planner's device programs
+executed by a NumPy emulator of the kernels' descriptor semantics vs the oracle."""
+
+import json
+
+import numpy as np
+import pytest
+
+import plan_emulator as em
+from circuits import random_circuit, random_observable
+from oracle import qcflow_port as orc
+from paper_2003_02989_b200 import gates as G
+from paper_2003_02989_b200 import planner as pl
+from paper_2003_02989_b200 import workloads as wl
+from paper_2003_02989_b200.circuit import Circuit, ParamExpr, circuit_symbols, from_json, gate_matrix, resolve, to_json
+from paper_2003_02989_b200.pauli import PauliString, PauliSum, pauli_sum_to_obj
+
+
+def test_gate_library_matches_oracle_gate_matrix():
+    rng = np.random.default_rng(0)
+    for fn in (G.rx, G.ry, G.rz, G.xpow, G.ypow, G.zpow):
+        g = fn(float(rng.uniform(-3, 3)), 0)
+        np.testing.assert_allclose(gate_matrix(g), orc.gate_matrix(g), atol=1e-13)
+    g = G.cnot_pow(0.37, 1, 0)
+    np.testing.assert_allclose(gate_matrix(g), orc.gate_matrix(g), atol=1e-13)
+    np.testing.assert_allclose(gate_matrix(G.cnot_pow(1.0, 0, 1)), G.FIXED_MATRICES["cnot"], atol=1e-13)
+    np.testing.assert_allclose(gate_matrix(G.xpow(1.0, 0)), G.FIXED_MATRICES["x"], atol=1e-13)
+
+
+def test_json_round_trip_and_errors():
+    rng = np.random.default_rng(1)
+    c = random_circuit(rng, 5, 30, n_sym=3)
+    c2 = from_json(to_json(c))
+    assert c2.num_qubits == c.num_qubits and len(c2) == len(c)
+    assert circuit_symbols(c2) == circuit_symbols(c)
+    with pytest.raises(ValueError, match="gates\\[0\\]"):
+        from_json('{"num_qubits": 2, "gates": [{"targets": [0]}]}')
+    with pytest.raises(ValueError, match="invalid JSON"):
+        from_json("{")
+    with pytest.raises(KeyError):
+        resolve(c, {})
+
+
+def test_workload_recipes_match_reference_built_circuits(golden):
+    meta, _ = golden
+    cfg = meta["configs"]
+    assert json.loads(to_json(wl.hea_circuit(6, 2))) == json.loads(cfg["hea"]["circuit"])
+    qa, cost = wl.qaoa_circuit(10, 2, [tuple(e) for e in cfg["qaoa"]["edges"]])
+    assert json.loads(to_json(qa)) == json.loads(cfg["qaoa"]["circuit"])
+    assert pauli_sum_to_obj(cost) == json.loads(cfg["qaoa"]["observable"])
+    assert json.loads(to_json(wl.brickwork_circuit(10, 6, seed=401))) == json.loads(cfg["rcs"]["circuit"])
+
+
+def _check_program(circ, obs, n, theta, adjoint_obs_diag=True):
+    syms = circuit_symbols(circ)
+    si = {s: i for i, s in enumerate(syms)}
+    infos = pl.analyse(circ, si)
+    diag = all(all(p == "Z" for p in t.factors.values()) for t in obs.terms)
+    nonid = PauliSum([t for t in obs.terms if t.factors])
+    prog = pl.build_program(circ, infos, n, adjoint=False, observables=[nonid], obs_diag_ids=[0] if diag else [])
+    em.check_invariants(prog)
+    fixed, consts = pl.concrete_tables([circ], infos)
+    mats, angs = em.build_tables(prog, theta, fixed, consts)
+    coefs = np.array([t.coefficient for t in nonid.terms])
+    psi, slots = em.run_forward(prog, mats, angs, theta.shape[0], n, coefs)
+    ident = sum(t.coefficient for t in obs.terms if not t.factors)
+    for b in range(theta.shape[0]):
+        bind = dict(zip(syms, theta[b]))
+        ref = orc.simulate_amps(circ, bind)
+        np.testing.assert_allclose(psi[b, : 1 << circ.num_qubits], ref, atol=1e-12)
+        if diag:
+            E = em.slots_to_cols(slots, prog.obs_slots, 1)[b, 0] + ident
+            assert E == pytest.approx(orc.expectation(ref, obs, circ.num_qubits), abs=1e-10)
+    if not syms or not diag:
+        return prog
+    infos_a = pl.analyse(circ, si)
+    adj = pl.build_program(circ, infos_a, n, adjoint=True, observables=[nonid], lam_diag=True)
+    em.check_invariants(adj)
+    fixed, consts = pl.concrete_tables([circ], infos_a)
+    mats_a, angs_a = em.build_tables(adj, theta, fixed, consts)
+    sl = em.run_adjoint(adj, mats_a, angs_a, theta.shape[0], n, psi, None, np.tile(coefs, (theta.shape[0], 1)))
+    grads = em.slots_to_cols(sl, adj.grad_slots, len(syms))
+    for b in range(theta.shape[0]):
+        _, g = orc.adjoint_grad(circ, obs, dict(zip(syms, theta[b])))
+        np.testing.assert_allclose(grads[b], g, atol=1e-5)  # float32 generator weights in the program
+    return prog
+
+
+@pytest.mark.parametrize("seed,n", [(0, 10), (1, 11), (2, 13), (3, 14), (4, 15), (5, 6)])
+def test_planner_programs_emulated_vs_oracle(seed, n):
+    rng = np.random.default_rng(seed)
+    circ = random_circuit(rng, n, 90, n_sym=4)
+    n_eff = max(n, pl.N_MIN)
+    theta = rng.uniform(-3, 3, size=(2, len(circuit_symbols(circ))))
+    _check_program(circ, random_observable(rng, n, diag=True), n_eff, theta)
+
+
+def test_planner_qaoa_pass_structure():
+    circ, cost = wl.qaoa_circuit(20, 4, wl.qaoa_graph(20))
+    si = {s: i for i, s in enumerate(circuit_symbols(circ))}
+    prog = pl.build_program(circ, pl.analyse(circ, si), 20, adjoint=False, observables=[cost], obs_diag_ids=[0])
+    adj = pl.build_program(circ, pl.analyse(circ, si), 20, adjoint=True, observables=[cost], lam_diag=True)
+    # p+1 passes is the minimum for 20 qubits with 13-qubit tiles (SURVEY 8(d) pass-count targets)
+    assert prog.stats["passes"] == 5 and prog.stats["product_init"] == 20
+    assert adj.stats["passes"] == 5
+
+
+def test_planner_qaoa_small_emulated():
+    circ, cost = wl.qaoa_circuit(14, 2, wl.qaoa_graph(14, seed=2))
+    _check_program(circ, cost, 14, wl.qaoa_params(2, 2).astype(np.float64))
+
+
+def test_planner_qcnn_and_brickwork_emulated():
+    model = wl.qcnn_model(8)
+    data = wl.qcnn_data_circuit(np.linspace(-3, 3, 8))
+    full = Circuit(8, tuple(data.gates) + tuple(model.gates))
+    rng = np.random.default_rng(9)
+    theta = rng.uniform(0, 2, size=(1, len(circuit_symbols(full))))
+    _check_program(full, PauliSum([PauliString(1.0, {7: "Z"})]), 10, theta)
+    bw = wl.brickwork_circuit(12, 5, seed=3)
+    _check_program(bw, wl.z_sum(12), 12, np.zeros((1, 0)))
