@@ -158,7 +158,7 @@ def test_sampler_bit_exact_on_identical_states(cuda):
     rng = np.random.default_rng(11)
     for n in (10, 13, 16):
         c = random_circuit(rng, n, 80)
-        psi = ops.state([c] * 3, [], np.zeros((3, 0), dtype=np.float32))
+        psi = ops.state([c] * 3, [], torch.zeros((3, 0), device="cuda"))
         seeds = [3, 99, 123456]
         idx, near = sample_indices(psi.contiguous(), n, 700, [philox_key(s) for s in seeds])
         st = psi.cpu().numpy().astype(np.complex128)
