@@ -273,6 +273,9 @@ def run_gpu(args, rank, world):
     struct_a = nat.QfProgram.from_buffer_copy(ad.struct)
     struct_a.coef_row_stride = hw.shape[1]
     fb, ab = pass_bytes(fw.prog, B), pass_bytes(ad.prog, B)
+    jf, ja = fw.jit(dev, B), ad.jit(dev, B)
+    kname = ("plan-specialised NVRTC tile-pass kernels qf_f_p*/qf_a_p* (forward L13/R5, adjoint L12/R4)"
+             if jf is not None else "qf::pass_kernel (forward L13/R5 + adjoint L12/R4)")
     reps = 3
     times_f = np.zeros(len(fb))
     times_a = np.zeros(len(ab))
@@ -280,12 +283,20 @@ def run_gpu(args, rank, world):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(fb) + len(ab) + 1)]
         ev[0].record(stream)
         for p in range(len(fb)):
-            nat.check(lib.qf_run_passes(C.byref(fw.struct), p, p + 1, _ptr(psi), n_eff, B, _ptr(mats_f),
-                                        _ptr(angs_f), _ptr(bound.fwd_coefs), _ptr(part_f), fw.tiles, s))
+            if jf is not None:
+                jf.run(B, _ptr(psi), 0, _ptr(mats_f), _ptr(angs_f), _ptr(bound.fwd_coefs), 0, _ptr(part_f), s,
+                       first=p, last=p + 1)
+            else:
+                nat.check(lib.qf_run_passes(C.byref(fw.struct), p, p + 1, _ptr(psi), n_eff, B, _ptr(mats_f),
+                                            _ptr(angs_f), _ptr(bound.fwd_coefs), _ptr(part_f), fw.tiles, s))
             ev[1 + p].record(stream)
         for p in range(len(ab)):
-            nat.check(lib.qf_adjoint_passes(C.byref(struct_a), p, p + 1, _ptr(psi), _ptr(lam), n_eff, B,
-                                            _ptr(mats_a), _ptr(angs_a), _ptr(hw), _ptr(part_a), ad.tiles, s))
+            if ja is not None:
+                ja.run(B, _ptr(psi), _ptr(lam), _ptr(mats_a), _ptr(angs_a), _ptr(hw), hw.shape[1], _ptr(part_a), s,
+                       first=p, last=p + 1)
+            else:
+                nat.check(lib.qf_adjoint_passes(C.byref(struct_a), p, p + 1, _ptr(psi), _ptr(lam), n_eff, B,
+                                                _ptr(mats_a), _ptr(angs_a), _ptr(hw), _ptr(part_a), ad.tiles, s))
             ev[1 + len(fb) + p].record(stream)
         torch.cuda.synchronize(dev)
         if r == 0:
@@ -346,7 +357,7 @@ def run_gpu(args, rank, world):
                     "d2h_bytes_per_step": int(BATCH * (1 + len(syms)) * 8)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "qf::pass_kernel (forward L13/R5 + adjoint L12/R4)",
+                         "kernel": kname,
                          "algorithmic_bytes_per_step": tot_bytes, "kernel_ms_per_step": tot_ms,
                          "pass_ms": [round(x, 4) for x in list(times_f) + list(times_a)],
                          "pass_gbs": [round(b / (t / 1000) / 1e9, 1) for b, t in

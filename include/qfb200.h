@@ -25,6 +25,7 @@
 #ifndef QFB200_H
 #define QFB200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -172,6 +173,21 @@ int qf_pauli_apply(const float* psi, float* lam, int n, int rows, int n_terms,
  * Philox starts at counter 1), out_idx [rows, shots] int64.  scratch: >= rows*(2^n/1024+2) doubles. */
 int qf_sample(const float* psi, int n, int rows, int shots, const uint64_t* keys,
               double* scratch, int64_t* out_idx, int32_t* near_boundary, void* stream);
+
+/* ---- plan-specialised kernels (jit.py generates CUDA source from the descriptors above) ---- */
+
+/* NVRTC-compile `src` (libnvrtc.so.12 loaded at run time) into a cubin; free with qf_jit_free. */
+int qf_jit_compile(const char* src, const char* name, const char* const* opts, int nopts, void** image,
+                   size_t* size);
+void qf_jit_free(void* p);
+/* Load a cubin into the current (primary) context; look up a kernel; unload. */
+int qf_jit_load(const void* image, void** module);
+int qf_jit_function(void* module, const char* name, int max_dyn_smem, void** func);
+int qf_jit_unload(void* module);
+/* Launch n generated pass kernels in order on `stream` with one packed argument struct
+ * (QfJitArgs in csrc/qf_jit_prelude.cuh). */
+int qf_jit_run(void* const* funcs, const uint32_t* grid, const uint32_t* block, const uint32_t* smem, int n,
+               void* stream, const void* args, size_t args_size);
 
 #ifdef __cplusplus
 }

@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libqfb200.so")
 EXPORTS = (
     "qf_last_error", "qf_version", "qf_device_sm_count", "qf_build_ops", "qf_run_passes",
     "qf_adjoint_passes", "qf_reduce_slots", "qf_pauli_expect", "qf_pauli_apply", "qf_sample",
+    "qf_jit_compile", "qf_jit_free", "qf_jit_load", "qf_jit_function", "qf_jit_unload", "qf_jit_run",
 )
 
 _p = C.c_void_p
@@ -72,8 +73,16 @@ def load(build_if_missing: bool = True):
     lib.qf_pauli_expect.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _i64, _p, _p]
     lib.qf_pauli_apply.argtypes = [_p, _p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _i64, _p]
     lib.qf_sample.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p]
+    lib.qf_jit_compile.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_char_p), C.c_int, C.POINTER(C.c_void_p),
+                                   C.POINTER(C.c_size_t)]
+    lib.qf_jit_free.argtypes = [_p]
+    lib.qf_jit_load.argtypes = [_p, C.POINTER(C.c_void_p)]
+    lib.qf_jit_function.argtypes = [_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
+    lib.qf_jit_unload.argtypes = [_p]
+    lib.qf_jit_run.argtypes = [_p, _p, _p, _p, C.c_int, _p, _p, C.c_size_t]
     for name in EXPORTS:
         getattr(lib, name).restype = C.c_int if name != "qf_last_error" else C.c_char_p
+    lib.qf_jit_free.restype = None
     _lib = lib
     return lib
 

@@ -70,6 +70,7 @@ class DeviceProgram:
         self.n_dense = len(r["dense_mat"])
         self.n_terms = len(r["term_beta"])
         self.tiles = 1 << (prog.n - prog.L)
+        self._jit = None
 
     def recipe(self, fixed_t, fixed_rows, const_t, const_rows) -> nat.QfBuildRecipe:
         a = self.r_arrays
@@ -83,6 +84,18 @@ class DeviceProgram:
             term_const=_ptr(const_t), const_rows=const_rows, n_const=max(self.n_const, 1),
         )
 
+    def jit(self, device, rows: int):
+        """Plan-specialised kernels for this program (compiled on first use) or None."""
+        from . import jit as _jit
+
+        if not _jit.enabled(rows, self.prog.n):
+            return None
+        if self._jit is None:
+            with _JIT_LOCK:
+                if self._jit is None:
+                    self._jit = _jit.JitProgram(self.prog, device.index or 0)
+        return self._jit
+
     def csr(self, mapping: dict, n_cols: int):
         ptr = [0]
         lst = []
@@ -92,6 +105,8 @@ class DeviceProgram:
         return (torch.tensor(ptr, dtype=torch.int32, device=self.device),
                 torch.tensor(lst or [0], dtype=torch.int32, device=self.device))
 
+
+_JIT_LOCK = threading.Lock()
 
 _TORCH_OF = {
     np.dtype(np.int32): torch.int32, np.dtype(np.float64): torch.float64,
@@ -273,8 +288,13 @@ class Bound:
         nat.check(lib.qf_build_ops(C.byref(rec), _ptr(theta), theta.shape[1], B, _ptr(mats), fw.prog.n_mat,
                                    _ptr(angs), fw.prog.n_ang, stream))
         partials = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
-        nat.check(lib.qf_run_passes(C.byref(fw.struct), 0, len(fw.prog.passes), _ptr(psi), n_eff, B, _ptr(mats),
-                                    _ptr(angs), _ptr(self.fwd_coefs), _ptr(partials), fw.tiles, stream))
+        jf = fw.jit(dev, B)
+        if jf is not None:
+            jf.run(B, _ptr(psi), 0, _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), 0, _ptr(partials), stream)
+        else:
+            nat.check(lib.qf_run_passes(C.byref(fw.struct), 0, len(fw.prog.passes), _ptr(psi), n_eff, B,
+                                        _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), _ptr(partials), fw.tiles,
+                                        stream))
         out: dict = {}
         if self.n_obs and want_expect:
             expv = torch.zeros((B, self.n_obs), dtype=torch.float64, device=dev)
@@ -324,11 +344,17 @@ class Bound:
                                              _ptr(ny), _ptr(hw_t), hw_t.shape[1], stream))
             else:
                 lam.zero_()
-        struct = nat.QfProgram.from_buffer_copy(ad.struct)
-        struct.coef_row_stride = hw_t.shape[1]
         partials = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
-        nat.check(lib.qf_adjoint_passes(C.byref(struct), 0, len(ad.prog.passes), _ptr(psi), _ptr(lam), n_eff, B,
-                                        _ptr(mats), _ptr(angs), _ptr(hw_t), _ptr(partials), ad.tiles, stream))
+        ja = ad.jit(dev, B)
+        if ja is not None:
+            ja.run(B, _ptr(psi), _ptr(lam), _ptr(mats), _ptr(angs), _ptr(hw_t), hw_t.shape[1], _ptr(partials),
+                   stream)
+        else:
+            struct = nat.QfProgram.from_buffer_copy(ad.struct)
+            struct.coef_row_stride = hw_t.shape[1]
+            nat.check(lib.qf_adjoint_passes(C.byref(struct), 0, len(ad.prog.passes), _ptr(psi), _ptr(lam), n_eff,
+                                            B, _ptr(mats), _ptr(angs), _ptr(hw_t), _ptr(partials), ad.tiles,
+                                            stream))
         grad = torch.zeros((B, max(self.S, 1)), dtype=torch.float64, device=dev)
         if self.S:
             ptr, lst = self.grad_csr

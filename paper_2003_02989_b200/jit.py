@@ -1,0 +1,409 @@
+"""Plan-specialised tile-pass kernels.
+
+The interpreted ``qf::pass_kernel`` reads the program descriptors at run time; ncu
+showed its cost is dominated by descriptor decode, op dispatch over many template
+instantiations (instruction-cache misses) and per-op warp reductions, not by the
+gate arithmetic.  This module emits, from exactly the same planner.Program, one
+straight-line CUDA kernel per pass in which every register slot, matrix-class,
+matrix offset, phase-polynomial mask and register subset, swizzled shared-memory
+offset and gradient slot is a compile-time constant; libqfb200's ``qf_jit_*``
+entry points compile it with NVRTC (sm_100a) and launch it.  Only per-row numbers
+(gate matrices, angles, observable coefficients) are read at run time.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import os
+import threading
+
+import numpy as np
+
+from . import _native as nat
+from . import planner as pl
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_PRELUDE = None
+_CACHE: dict = {}
+_LOCK = threading.Lock()
+
+
+def prelude() -> str:
+    global _PRELUDE
+    if _PRELUDE is None:
+        with open(os.path.join(_HERE, "csrc", "qf_jit_prelude.cuh")) as f:
+            _PRELUDE = f.read()
+    return _PRELUDE
+
+
+class QfJitArgs(C.Structure):
+    _fields_ = [("psi", C.c_void_p), ("lam", C.c_void_p), ("mats", C.c_void_p), ("angles", C.c_void_p),
+                ("coefs", C.c_void_p), ("partials", C.c_void_p), ("n_mat", C.c_int), ("n_ang", C.c_int),
+                ("coef_stride", C.c_int), ("n_slots", C.c_int), ("tiles_log2", C.c_int), ("pad", C.c_int)]
+
+
+def _flit(x: float) -> str:
+    return repr(float(np.float32(x))) + "f"
+
+
+def _xor_expr(bits: list, var: str = "t") -> str:
+    """XOR over thread bits i of (t bit i ? c_i : 0) with c_i literal."""
+    parts = [f"((({var}) >> {i}) & 1u ? {c}u : 0u)" for i, c in enumerate(bits) if c]
+    return "(" + " ^ ".join(parts) + ")" if parts else "0u"
+
+
+def _wht_code(vals: dict, R: int, kind: str, out: str, indent: str) -> list:
+    """Walsh-Hadamard transform over 2^R entries with symbolic zero tracking.
+    vals: S -> variable name (entries absent are zero).  Emits `out{r}` variables."""
+    lines = []
+    cur = {S: v for S, v in vals.items()}
+    tmp_id = [0]
+    for j in range(R):
+        nxt = {}
+        for r in range(1 << R):
+            if r & (1 << j):
+                continue
+            x, y = cur.get(r), cur.get(r | (1 << j))
+            if x is None and y is None:
+                continue
+            a = f"{out}_{j}_{r}"
+            b = f"{out}_{j}_{r | (1 << j)}"
+            if y is None:
+                lines.append(f"{indent}const {kind} {a} = {x}, {b} = {x};")
+            elif x is None:
+                neg = f"(0u - {y})" if kind == "u32" else f"(-{y})"
+                lines.append(f"{indent}const {kind} {a} = {y}, {b} = {neg};")
+            else:
+                lines.append(f"{indent}const {kind} {a} = {x} + {y}, {b} = {x} - {y};")
+            nxt[r] = a
+            nxt[r | (1 << j)] = b
+        cur = nxt
+    zero = "0u" if kind == "u32" else "0.f"
+    for r in range(1 << R):
+        lines.append(f"{indent}const {kind} {out}{r} = {cur.get(r, zero)};")
+    return lines
+
+
+def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
+    """Per-pass CUDA kernel sources (without prelude), kernel names, launch geometry."""
+    n, L, R, adj = prog.n, prog.L, prog.R, prog.adjoint
+    TB = L - R
+    NR, NT = 1 << R, 1 << TB
+    NA = 2 if adj else 1
+    TILE = 1 << L
+    minb = max(1, min(8, 65536 // (NT * 128)))
+    gm = prog.genmats.reshape(-1, 2) if len(prog.genmats) else np.zeros((0, 2), np.float32)
+    src = []
+    names, geo = [], []
+    for pi, p in enumerate(prog.passes):
+        name = f"qf_{tag}_p{pi}"
+        names.append(name)
+        sb, se = int(p[0]), int(p[1])
+        init, store = int(p[2]), int(p[3])
+        mb, me = int(p[4]), int(p[5])
+        ab, ae = int(p[6]), int(p[7])
+        slb, sle = int(p[8]), int(p[9])
+        n_out = int(p[10])
+        cb, ce = int(p[11]), int(p[12])
+        outer = [int(x) for x in p[16:16 + n_out]]
+        init_mat = [int(x) for x in p[48:48 + n]]
+        mcnt, acnt, ccnt, scnt = me - mb, ae - ab, ce - cb, sle - slb
+        smem = NA * TILE * 8 + mcnt * 8 + acnt * 4 + ccnt * 4 + scnt * NT * 4 + 16
+        geo.append((NT, smem))
+        o = []
+        w = o.append
+        w(f'extern "C" __global__ void __launch_bounds__({NT}, {minb}) {name}(const QfJitArgs a) {{')
+        w("  extern __shared__ __align__(16) unsigned char smem_raw[];")
+        w("  float2* sm = reinterpret_cast<float2*>(smem_raw);")
+        w(f"  float2* M = sm + {NA * TILE};")
+        w(f"  int* ANG = reinterpret_cast<int*>(M + {mcnt});")
+        w(f"  float* CO = reinterpret_cast<float*>(ANG + {acnt});")
+        w(f"  float* GS = CO + {ccnt};")
+        w("  const u32 t = threadIdx.x;")
+        w(f"  const int row = (int)(blockIdx.x >> {n - L});")
+        w(f"  const u32 o = blockIdx.x & {(1 << (n - L)) - 1}u;")
+        if mcnt:
+            w(f"  for (int i = t; i < {mcnt}; i += {NT}) M[i] = a.mats[(size_t)row * a.n_mat + {mb} + i];")
+        if acnt:
+            w(f"  for (int i = t; i < {acnt}; i += {NT}) ANG[i] = a.angles[(size_t)row * a.n_ang + {ab} + i];")
+        if ccnt:
+            w(f"  for (int i = t; i < {ccnt}; i += {NT}) CO[i] = a.coefs[(size_t)row * a.coef_stride + {cb} + i];")
+        base = " | ".join(f"(((o >> {i}) & 1u) << {q})" for i, q in enumerate(outer)) or "0u"
+        w(f"  const u32 base = {base};")
+        w(f"  float2* __restrict__ psi = a.psi + ((size_t)row << {n});")
+        if adj:
+            w(f"  float2* __restrict__ lam = a.lam + ((size_t)row << {n});")
+        w(f"  float2 v0[{NR}];")
+        if adj:
+            w(f"  float2 v1[{NR}];")
+        w("  __syncthreads();")
+
+        st_rows = [prog.stages[s] for s in range(sb, se)]
+
+        def tglob(st):
+            return [1 << int(st[8 + i]) for i in range(TB)]
+
+        def tphys(st):
+            return [int(st[32 + i]) for i in range(TB)]
+
+        def roff(st, r, phys=False):
+            x = 0
+            for j in range(R):
+                if r >> j & 1:
+                    x ^= int(st[24 + j]) if phys else (1 << int(st[j]))
+            return x
+
+        # ---- load / init ----
+        st0 = st_rows[0]
+        w(f"  const u32 gt0 = base | {_xor_expr(tglob(st0))};")
+        if init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI):
+            for r in range(NR):
+                w(f"  v0[{r}] = psi[gt0 + {roff(st0, r)}u];")
+                if adj:
+                    w(f"  v1[{r}] = " + (f"lam[gt0 + {roff(st0, r)}u];" if init == pl.INIT_LOAD else
+                                          "make_float2(0.f, 0.f);"))
+        elif init == pl.INIT_ZERO:
+            w("  v0[0] = make_float2(gt0 == 0u ? 1.f : 0.f, 0.f);")
+            for r in range(1, NR):
+                w(f"  v0[{r}] = make_float2(0.f, 0.f);")
+        else:
+            regq = {int(st0[j]) for j in range(R)}
+            w("  float2 c = make_float2(1.f, 0.f);")
+            for q in range(n):
+                if q in regq:
+                    continue
+                mo = init_mat[q] if q < len(init_mat) else -1
+                if mo < 0:
+                    w(f"  if ((gt0 >> {q}) & 1u) c = make_float2(0.f, 0.f);")
+                else:
+                    w(f"  c = cmul(c, ((gt0 >> {q}) & 1u) ? M[{mo - mb + 2}] : M[{mo - mb}]);")
+            w("  v0[0] = c;")
+            for j in range(R):
+                mo = init_mat[int(st0[j])]
+                f0 = "make_float2(1.f, 0.f)" if mo < 0 else f"M[{mo - mb}]"
+                f1 = "make_float2(0.f, 0.f)" if mo < 0 else f"M[{mo - mb + 2}]"
+                w(f"  {{ const float2 f0 = {f0}, f1 = {f1};")
+                for r in range(1 << j):
+                    w(f"    v0[{r | (1 << j)}] = cmul(v0[{r}], f1); v0[{r}] = cmul(v0[{r}], f0);")
+                w("  }")
+
+        # ---- stages ----
+        for si, st in enumerate(st_rows):
+            if si:
+                prev = st_rows[si - 1]
+                w("  __syncthreads();")
+                w(f"  {{ const u32 tp = {_xor_expr(tphys(prev))};")
+                for r in range(NR):
+                    w(f"    sm[tp ^ {roff(prev, r, True)}u] = v0[{r}];")
+                    if adj:
+                        w(f"    sm[{TILE} + (tp ^ {roff(prev, r, True)}u)] = v1[{r}];")
+                w("  }")
+                w("  __syncthreads();")
+                w(f"  {{ const u32 tp = {_xor_expr(tphys(st))};")
+                for r in range(NR):
+                    w(f"    v0[{r}] = sm[tp ^ {roff(st, r, True)}u];")
+                    if adj:
+                        w(f"    v1[{r}] = sm[{TILE} + (tp ^ {roff(st, r, True)}u)];")
+                w("  }")
+            reg_glob = [int(st[j]) for j in range(R)]
+            need_gt = any(int(prog.ops[k][0]) in (pl.OP_DIAG, pl.OP_OBS) for k in range(int(st[48]), int(st[49])))
+            if need_gt:
+                w(f"  {{ const u32 gt = base | {_xor_expr(tglob(st))};")
+            else:
+                w("  {")
+            for k in range(int(st[48]), int(st[49])):
+                op = prog.ops[k]
+                kind = int(op[0])
+                s0, s1, moff = int(op[1]), int(op[2]), int(op[3]) - mb
+                slot = int(op[7])
+                cls, gk = int(op[9]), int(op[10])
+                if kind == pl.OP_DENSE1:
+                    w(f"    {{ float2 u00 = M[{moff}], u01 = M[{moff + 1}], u10 = M[{moff + 2}], u11 = M[{moff + 3}];")
+                    if adj:
+                        if slot >= 0:
+                            g0 = int(op[8])
+                            if gk:
+                                sc = float(gm[g0 + 4, 0])
+                                w(f"      const float gacc = {_flit(sc)} * gradp<{s0}, {NR}, {gk}>(v0, v1);")
+                            else:
+                                gl = [f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})" for i in range(4)]
+                                w(f"      const float gacc = grad1<{s0}, {NR}>(v0, v1, {', '.join(gl)});")
+                            w(f"      GS[{(slot - slb) * NT} + t] = gacc;")
+                        w("      { const float2 x = u01; u00.y = -u00.y; u11.y = -u11.y;"
+                          " u01 = make_float2(u10.x, -u10.y); u10 = make_float2(x.x, -x.y); }")
+                        w(f"      apply1<{s0}, {NR}, {cls}>(v1, u00, u01, u10, u11);")
+                    w(f"      apply1<{s0}, {NR}, {cls}>(v0, u00, u01, u10, u11); }}")
+                elif kind == pl.OP_DENSE2:
+                    if adj:
+                        w(f"    {{ float2 m[16]; for (int i = 0; i < 4; ++i) for (int j = 0; j < 4; ++j) "
+                          f"{{ const float2 x = M[{moff} + j * 4 + i]; m[i * 4 + j] = make_float2(x.x, -x.y); }}")
+                        if slot >= 0:
+                            g0 = int(op[8])
+                            gl = ", ".join(f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})"
+                                           for i in range(16))
+                            w(f"      const float2 g[16] = {{{gl}}};")
+                            w(f"      GS[{(slot - slb) * NT} + t] = grad2<{s0}, {s1}, {NR}>(v0, v1, g);")
+                        w(f"      apply2<{s0}, {s1}, {NR}>(v0, m); apply2<{s0}, {s1}, {NR}>(v1, m); }}")
+                    else:
+                        w(f"    {{ float2 m[16]; for (int i = 0; i < 16; ++i) m[i] = M[{moff} + i];")
+                        w(f"      apply2<{s0}, {s1}, {NR}>(v0, m); }}")
+                elif kind in (pl.OP_DIAG, pl.OP_OBS):
+                    tb, te = int(op[4]), int(op[5])
+                    groups: dict = {}
+                    for kk in range(tb, te):
+                        S = pl._bit_subset(int(prog.term_mask[kk]), reg_glob)
+                        groups.setdefault(S, []).append(kk)
+                    pre = f"d{k}"
+                    w("    {")
+                    if kind == pl.OP_DIAG:
+                        if adj and slot >= 0:
+                            # gradient: sum_S W[S] * B[S], W = WHT(Im(conj(lam) psi)), B[S] = sum w_k sign_k
+                            for r in range(NR):
+                                w(f"      const float {pre}w{r} = im_conj_mul(v1[{r}], v0[{r}]);")
+                            wl = _wht_code({r: f"{pre}w{r}" for r in range(NR)}, R, "float", f"{pre}W", "      ")
+                            o.extend(wl)
+                            terms_acc = []
+                            for S, ks in groups.items():
+                                acc = f"{pre}b{S}"
+                                w(f"      float {acc} = 0.f;")
+                                for kk in ks:
+                                    wt = float(prog.term_w[kk])
+                                    if wt == 0.0:
+                                        continue
+                                    m = int(prog.term_mask[kk])
+                                    w(f"      {acc} += (__popc(gt & {m}u) & 1) ? {_flit(-wt)} : {_flit(wt)};")
+                                terms_acc.append(f"{pre}W{S} * {acc}")
+                            w(f"      GS[{(slot - slb) * NT} + t] = {' + '.join(terms_acc) or '0.f'};")
+                        for S, ks in groups.items():
+                            w(f"      u32 {pre}a{S} = 0u;")
+                            for kk in ks:
+                                m = int(prog.term_mask[kk])
+                                col = int(prog.term_idx[kk]) - ab
+                                w(f"      {{ const u32 x = (u32)ANG[{col}]; {pre}a{S} += (__popc(gt & {m}u) & 1) ? (0u - x) : x; }}")
+                        o.extend(_wht_code({S: f"{pre}a{S}" for S in groups}, R, "u32", f"{pre}A", "      "))
+                        for r in range(NR):
+                            w(f"      {{ const float2 ph = phase_turns((int){pre}A{r}, {'true' if adj else 'false'});"
+                              f" v0[{r}] = cmul(v0[{r}], ph);" + (f" v1[{r}] = cmul(v1[{r}], ph);" if adj else "") + " }")
+                    else:  # OBS
+                        for S, ks in groups.items():
+                            w(f"      float {pre}a{S} = 0.f;")
+                            for kk in ks:
+                                m = int(prog.term_mask[kk])
+                                col = -1 - int(prog.term_idx[kk]) - cb
+                                w(f"      {{ const float x = CO[{col}]; {pre}a{S} += (__popc(gt & {m}u) & 1) ? -x : x; }}")
+                        o.extend(_wht_code({S: f"{pre}a{S}" for S in groups}, R, "float", f"{pre}A", "      "))
+                        w("      float e = 0.f;")
+                        for r in range(NR):
+                            w(f"      e = fmaf({pre}A{r}, fmaf(v0[{r}].x, v0[{r}].x, v0[{r}].y * v0[{r}].y), e);")
+                            if adj:
+                                w(f"      v1[{r}] = cscale({pre}A{r}, v0[{r}]);")
+                        if slot >= 0:
+                            w(f"      GS[{(slot - slb) * NT} + t] = e;")
+                    w("    }")
+            w("  }")
+
+        # ---- store ----
+        if store:
+            stl = st_rows[-1]
+            w(f"  {{ const u32 gs = base | {_xor_expr(tglob(stl))};")
+            for r in range(NR):
+                w(f"    psi[gs + {roff(stl, r)}u] = v0[{r}];")
+                if adj:
+                    w(f"    lam[gs + {roff(stl, r)}u] = v1[{r}];")
+            w("  }")
+        if scnt:
+            w("  __syncthreads();")
+            w(f"  for (int s = t >> 5; s < {scnt}; s += {max(NT // 32, 1)}) {{")
+            w("    double acc = 0.0;")
+            w(f"    for (int i = (t & 31); i < {NT}; i += 32) acc += (double)GS[s * {NT} + i];")
+            w("    acc = warp_sum_d(acc);")
+            w(f"    if ((t & 31) == 0) a.partials[((size_t)row * a.n_slots + {slb} + s) * {1 << (n - L)} + o] = acc;")
+            w("  }")
+        w("}")
+        src.append("\n".join(o) + "\n")
+    return src, names, geo
+
+
+_OPTS = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", b"--device-as-default-execution-space"]
+
+
+def _cache_dir() -> str:
+    d = os.environ.get("QF_JIT_CACHE", os.path.join(os.path.expanduser("~"), ".cache", "qfb200"))
+    os.makedirs(d, exist_ok=True)
+    return d
+
+
+def compile_kernel(source: str, name: str) -> bytes:
+    """NVRTC-compile one kernel (prelude + body) to an sm_100a cubin, with a disk cache."""
+    full = prelude() + "\n" + source
+    key = hashlib.sha256(full.encode() + b"|".join(_OPTS)).hexdigest()
+    path = os.path.join(_cache_dir(), key + ".cubin")
+    if os.path.exists(path):
+        with open(path, "rb") as f:
+            return f.read()
+    lib = nat.load()
+    arr = (C.c_char_p * len(_OPTS))(*_OPTS)
+    img = C.c_void_p()
+    size = C.c_size_t()
+    nat.check(lib.qf_jit_compile(full.encode(), (name + ".cu").encode(), arr, len(_OPTS), C.byref(img),
+                                 C.byref(size)))
+    image = C.string_at(img, size.value)
+    lib.qf_jit_free(img)
+    tmp = path + f".{os.getpid()}.tmp"
+    with open(tmp, "wb") as f:
+        f.write(image)
+    os.replace(tmp, path)
+    return image
+
+
+class JitProgram:
+    """Compiled, loaded kernels of one planner.Program (one module per pass, compiled in parallel)."""
+
+    def __init__(self, prog: pl.Program, device_index: int):
+        from concurrent.futures import ThreadPoolExecutor
+
+        lib = nat.load()
+        tag = "a" if prog.adjoint else "f"
+        sources, names, geo = generate(prog, tag)
+        with ThreadPoolExecutor(max_workers=min(len(sources), os.cpu_count() or 4)) as ex:
+            images = list(ex.map(lambda a: compile_kernel(*a), zip(sources, names)))
+        self.modules, funcs = [], []
+        for img, nm, (_, smem) in zip(images, names, geo):
+            mod = C.c_void_p()
+            nat.check(lib.qf_jit_load(img, C.byref(mod)))
+            f = C.c_void_p()
+            nat.check(lib.qf_jit_function(mod, nm.encode(), max(smem, 48 * 1024), C.byref(f)))
+            self.modules.append(mod)
+            funcs.append(f.value)
+        P = len(names)
+        self.n = P
+        self.names = names
+        self.funcs = (C.c_void_p * P)(*funcs)
+        self.rows_shift = prog.n - prog.L
+        self.block = (C.c_uint32 * P)(*[g[0] for g in geo])
+        self.smem = (C.c_uint32 * P)(*[g[1] for g in geo])
+        self.grid = (C.c_uint32 * P)()
+        self.prog = prog
+
+    def run(self, rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first=0, last=None):
+        lib = nat.load()
+        last = self.n if last is None else last
+        args = QfJitArgs(psi=psi, lam=lam, mats=mats, angles=angles, coefs=coefs, partials=partials,
+                         n_mat=self.prog.n_mat, n_ang=self.prog.n_ang, coef_stride=coef_stride,
+                         n_slots=self.prog.n_slots, tiles_log2=self.rows_shift, pad=0)
+        for i in range(self.n):
+            self.grid[i] = rows << self.rows_shift
+        cnt = last - first
+        nat.check(lib.qf_jit_run(C.addressof(self.funcs) + C.sizeof(C.c_void_p) * first,
+                                 C.addressof(self.grid) + 4 * first, C.addressof(self.block) + 4 * first,
+                                 C.addressof(self.smem) + 4 * first, cnt, stream, C.byref(args), C.sizeof(args)))
+
+
+def enabled(rows: int, n_eff: int) -> bool:
+    """Plan-specialised kernels pay off once a launch moves enough data to amortise the
+    one-off NVRTC compile; QF_JIT=1/0 forces them on/off."""
+    flag = os.environ.get("QF_JIT")
+    if flag is not None:
+        return flag not in ("0", "", "false", "no")
+    return rows * (1 << n_eff) >= (1 << 24)

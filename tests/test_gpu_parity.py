@@ -312,3 +312,29 @@ def test_rcs24_sampling_bit_exact(cuda):
         np.testing.assert_array_equal(bits[b], want)
     norms = (np.abs(st) ** 2).sum(axis=1)
     np.testing.assert_allclose(norms, 1.0, atol=1e-5)
+
+
+def test_plan_specialised_kernels_match_interpreter(cuda, monkeypatch):
+    """The NVRTC-generated pass kernels (jit.py) and the interpreted pass kernel run the
+    same programs; both must agree with the oracle (forward, adjoint, fused observables)."""
+    rng = np.random.default_rng(21)
+    c = random_circuit(rng, 15, 160, n_sym=5)
+    syms = circuit_symbols(c)
+    theta = rng.uniform(-3, 3, size=(4, len(syms))).astype(np.float32)
+    obs = [random_observable(rng, 15, diag=True)]
+    out = {}
+    for flag in ("0", "1"):
+        monkeypatch.setenv("QF_JIT", flag)
+        from paper_2003_02989_b200.engine import ENGINE
+
+        ENGINE._bound.clear()
+        st = ops.state([c] * 4, syms, theta)
+        e, g = ops.expectation_and_gradient([c] * 4, syms, theta, obs)
+        out[flag] = (st, e, g)
+    np.testing.assert_allclose(out["1"][0], out["0"][0], atol=1e-6)
+    np.testing.assert_allclose(out["1"][1], out["0"][1], atol=1e-6)
+    np.testing.assert_allclose(out["1"][2], out["0"][2], atol=1e-5, rtol=1e-6)
+    bind = dict(zip(syms, theta[0].astype(np.float64)))
+    ee, gg = orc.adjoint_grad(c, obs[0], bind)
+    assert out["1"][1][0, 0] == pytest.approx(ee, abs=EXP)
+    _close_grad(out["1"][2][0], gg)
