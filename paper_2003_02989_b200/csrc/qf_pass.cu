@@ -550,6 +550,12 @@ int run_pass(const PassArgs& a, const QfPass& hp, bool adj, cudaStream_t stream)
       case 12: return launch_pass<12, 5, false>(a, hp, stream);
       case 13: return launch_pass<13, 5, false>(a, hp, stream);
     }
+  } else if (!adj && R == 4) {
+    switch (L) {
+      case 10: return launch_pass<10, 4, false>(a, hp, stream);
+      case 11: return launch_pass<11, 4, false>(a, hp, stream);
+      case 12: return launch_pass<12, 4, false>(a, hp, stream);
+    }
   } else if (adj && R == 4) {
     switch (L) {
       case 10: return launch_pass<10, 4, true>(a, hp, stream);

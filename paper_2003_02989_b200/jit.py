@@ -92,7 +92,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
     NR, NT = 1 << R, 1 << TB
     NA = 2 if adj else 1
     TILE = 1 << L
-    minb = max(1, min(8, 65536 // (NT * 128)))
+    minb = int(os.environ.get("QF_MINB_ADJ" if adj else "QF_MINB_FWD", "0")) or max(1, min(8, 65536 // (NT * (NR * 2 * NA + 32))))
     gm = prog.genmats.reshape(-1, 2) if len(prog.genmats) else np.zeros((0, 2), np.float32)
     src = []
     names, geo = [], []

@@ -31,8 +31,22 @@ from .pauli import term_masks
 
 N_MIN = 10          # smaller registers are padded (extra qubits stay |0>)
 LANE_Q = 4          # qubits 0..3 are always lane bits at load/store (128-byte runs)
-FWD_L, FWD_R = 13, 5
+FWD_L, FWD_R = 12, 4   # 4 CTAs/SM at 64 registers: measured faster than 13/5 at 2 CTAs/SM
 ADJ_L, ADJ_R = 12, 4
+
+
+
+def geometry(adjoint: bool) -> tuple:
+    """(L, R) of the tile passes; QF_GEOM_FWD / QF_GEOM_ADJ="L,R" override (experiments;
+    only the plan-specialised kernels support geometries other than the defaults)."""
+    import os
+
+    env = os.environ.get("QF_GEOM_ADJ" if adjoint else "QF_GEOM_FWD")
+    if env:
+        L, R = (int(x) for x in env.split(","))
+        return L, R
+    return (ADJ_L, ADJ_R) if adjoint else (FWD_L, FWD_R)
+
 
 OP_DENSE1, OP_DENSE2, OP_DIAG, OP_OBS = 1, 2, 3, 4
 CLS_GENERAL, CLS_XLIKE, CLS_REAL = 0, 1, 2   # dense 1q matrix structure classes
@@ -623,7 +637,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     OBS ops at the end of the forward program; ``lam_diag``: adjoint with a diagonal H
     whose lambda-init / energy is fused into the first backward pass; ``from_state``:
     the forward program starts from a caller-provided state instead of |0...0>."""
-    L, R = (ADJ_L, ADJ_R) if adjoint else (FWD_L, FWD_R)
+    L, R = geometry(adjoint)
     L = min(L, n)
     ops = build_ops(infos, adjoint)
     if from_state and not adjoint:
