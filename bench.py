@@ -267,6 +267,14 @@ def run_gpu(args, rank, world):
                                _ptr(angs_f), fw.prog.n_ang, s))
     nat.check(lib.qf_build_ops(C.byref(rec_a), _ptr(theta), theta.shape[1], B, _ptr(mats_a), ad.prog.n_mat,
                                _ptr(angs_a), ad.prog.n_ang, s))
+    if fw.frame:  # the same per-row Pauli-frame rewrite execute() performs
+        sc_f = torch.empty((B, max(fw.prog.n_slots, 1)), dtype=torch.float64, device=dev)
+        sc_a = torch.empty((B, max(ad.prog.n_slots, 1)), dtype=torch.float64, device=dev)
+        fr = torch.empty((B, 2), dtype=torch.float64, device=dev)
+        nat.check(lib.qf_frame_walk(_ptr(fw.t_events), fw.n_events, 0, B, _ptr(mats_f), fw.prog.n_mat, _ptr(angs_f),
+                                    fw.prog.n_ang, _ptr(sc_f), fw.prog.n_slots, None, _ptr(fr), s))
+        nat.check(lib.qf_frame_walk(_ptr(ad.t_events), ad.n_events, 1, B, _ptr(mats_a), ad.prog.n_mat, _ptr(angs_a),
+                                    ad.prog.n_ang, _ptr(sc_a), ad.prog.n_slots, _ptr(fr), None, s))
     part_f = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
     part_a = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
     hw = torch.ones((B, max(len(bound.hkeys), 1)), dtype=torch.float32, device=dev)

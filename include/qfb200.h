@@ -155,6 +155,30 @@ int qf_reduce_slots(const double* partials, int rows, int n_slots, int tiles,
                     const int32_t* col_ptr, const int32_t* slot_list, int n_cols, double* out,
                     int accumulate, void* stream);
 
+/* As qf_reduce_slots, each slot's sum multiplied by slot_scale[row, slot] (the Pauli-frame
+ * scale written by qf_frame_walk).  Same reference role as qf_reduce_slots. */
+int qf_reduce_slots_scaled(const double* partials, int rows, int n_slots, int tiles,
+                           const int32_t* col_ptr, const int32_t* slot_list, int n_cols, double* out,
+                           int accumulate, const double* slot_scale, void* stream);
+
+/* Per-row Pauli frame of a normalised program: true state = sqrt(m) X^x Z^z stored state
+ * (up to a global phase). */
+typedef struct QfFrame {
+  uint32_t x;
+  uint32_t z;
+  double m;
+} QfFrame;
+
+/* Pauli-frame walk over a program's events [n_events, 8] (planner.build_program frame=True),
+ * in execution order, one thread per row: rewrites normalised rotation matrices to their
+ * tau form, folds the frame into general dense matrices, writes the frame x-masks into the
+ * angle table and the slot scales [rows, n_slots].  frame_in (nullable) = the forward
+ * program's frame_out for the adjoint sweep.  Part of gate_matrix/fuse per row
+ * (qcflow/circuit.py:281-309, fusion.py:78-176): an exact re-factorisation, not a new op. */
+int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, float* mats, int n_mat,
+                  int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
+                  QfFrame* frame_out, void* stream);
+
 /* Generic Pauli-sum expectation partials: partials[row, k, chunk] = coef[row, k] *
  * sum_{x in chunk} Re(conj(psi[x ^ xm_k]) i^{ny_k} (-1)^{popc(x & zm_k)} psi[x]);
  * chunks = ceil(2^n / 2048).  Sum with qf_reduce_slots (slots = terms, tiles = chunks).

@@ -139,6 +139,10 @@ __global__ void build_angle_kernel(const QfBuildRecipe R, const float* theta, in
   const int row = (int)(id / R.n_terms), k = (int)(id % R.n_terms);
   const int kind = R.term_src[2 * k], src = R.term_src[2 * k + 1];
   double ang;
+  if (kind == 2) {  // frame x-mask column: filled by frame_walk_kernel
+    angles[(size_t)row * n_ang + k] = 0;
+    return;
+  }
   if (kind == 0) {
     const double v = R.gen_coeff[src] * (double)theta[row * tstride + R.gen_sym[src]] + R.gen_const[src];
     ang = v * R.term_beta[k];
@@ -157,7 +161,7 @@ __global__ void build_angle_kernel(const QfBuildRecipe R, const float* theta, in
 
 __global__ void reduce_slots_kernel(const double* __restrict__ partials, int rows, int n_slots, int tiles,
                                     const int32_t* col_ptr, const int32_t* slot_list, int n_cols,
-                                    double* out, int accumulate) {
+                                    double* out, int accumulate, const double* __restrict__ slot_scale) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows * n_cols) return;
@@ -167,7 +171,8 @@ __global__ void reduce_slots_kernel(const double* __restrict__ partials, int row
     const double* p = partials + ((size_t)row * n_slots + slot_list[s]) * tiles;
     double part = 0.0;
     for (int i = lane; i < tiles; i += 32) part += p[i];
-    acc += warp_sum_d(part);
+    part = warp_sum_d(part);
+    acc += slot_scale ? part * slot_scale[(size_t)row * n_slots + slot_list[s]] : part;
   }
   if (lane == 0) out[(size_t)row * n_cols + col] = accumulate ? out[(size_t)row * n_cols + col] + acc : acc;
 }
@@ -375,6 +380,118 @@ __global__ void draw_kernel(const float2* __restrict__ psi, int n, int rows, int
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Pauli-frame walk (one thread per row, events in program execution order).
+//
+// Invariant: true state = sqrt(m) * X^x Z^z * stored state (up to a global phase, which
+// cancels in every expectation and in Im<lambda|G|psi> because psi and lambda share it).
+//   EV_NX / EV_NY  the op applies A = P^dag U P (U = the built matrix, or U^dag in the
+//                  adjoint; P = frame on q).  A = e^{i phi}(c I - i s Q), Q = X or Y, is
+//                  written as (c)(I - i t Q) [|c| >= |s|] or (-i s Q)(I + i (c/s) Q), so the
+//                  kernel applies I - i tau Q with |tau| <= 1, m *= max(c^2, s^2) and the
+//                  second form multiplies the frame by Q.  Gradient slot scale = m * sign,
+//                  sign = (-1)^{z_q} (X) or (-1)^{x_q + z_q} (Y) = P^dag Q P / Q.
+//   EV_ABS1/ABS2   general dense op: matrix absorbs the frame (M P, or P M in the adjoint
+//                  whose kernels apply M^dag), frame bits on its qubits are cleared.
+//   EV_DIAG/OBS    frame x-mask written to the op's angle column (kernels evaluate the
+//                  phase polynomial / observable at index ^ x); slot scale = m.
+// ---------------------------------------------------------------------------
+
+__device__ void frame_pauli(int a, int b, Z (&P)[4]) {  // X^a Z^b, row-major 2x2
+  // Z^b = diag(1, (-1)^b);  X^a Z^b
+  const double zb = b ? -1.0 : 1.0;
+  if (!a) {
+    P[0] = {1, 0}; P[1] = {0, 0}; P[2] = {0, 0}; P[3] = {zb, 0};
+  } else {
+    P[0] = {0, 0}; P[1] = {zb, 0}; P[2] = {1, 0}; P[3] = {0, 0};
+  }
+}
+
+__global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int adjoint, int rows,
+                                  float2* mats, int n_mat, int32_t* angles, int n_ang, double* slot_scale,
+                                  int n_slots, const QfFrame* frame_in, QfFrame* frame_out) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  uint32_t x = 0, z = 0;
+  double m = 1.0;
+  if (frame_in) {
+    x = frame_in[row].x;
+    z = frame_in[row].z;
+    m = frame_in[row].m;
+  }
+  float2* M = mats + (size_t)row * n_mat;
+  for (int e = 0; e < n_ev; ++e) {
+    const int32_t* E = ev + (size_t)e * 8;
+    const int kind = E[0], q0 = E[1], q1 = E[2], off = E[3], slot = E[4], col = E[5];
+    if (kind == 1 || kind == 2) {  // normalised X / Y rotation on q0
+      const uint32_t bit = 1u << q0;
+      const int ax = (x & bit) ? 1 : 0, bz = (z & bit) ? 1 : 0;
+      const int flip = kind == 1 ? bz : (ax ^ bz);
+      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = flip ? -m : m;
+      Z u00 = {M[off].x, M[off].y}, u01 = {M[off + 1].x, M[off + 1].y}, u10 = {M[off + 2].x, M[off + 2].y};
+      if (adjoint) {  // kernels of the adjoint sweep apply U^dag
+        const Z t01 = u01;
+        u00.y = -u00.y;
+        u01 = {u10.x, -u10.y};
+        u10 = {t01.x, -t01.y};
+      }
+      // U = e^{i phi}(c I - i s Q):  X: u01 = -i e^{i phi} s;  Y: u10 = e^{i phi} s
+      const Z sv = kind == 1 ? Z{-u01.y, u01.x} /* i*u01 */ : u10;  // e^{i phi} s
+      const double c2 = u00.x * u00.x + u00.y * u00.y, s2 = sv.x * sv.x + sv.y * sv.y;
+      double tau;
+      if (c2 >= s2) {  // t = s / c (real up to rounding): Re(sv * conj(u00)) / |u00|^2
+        tau = (sv.x * u00.x + sv.y * u00.y) / c2;
+        if (flip) tau = -tau;
+        m *= c2;
+      } else {         // tau = -c/s
+        double k = (u00.x * sv.x + u00.y * sv.y) / s2;
+        if (flip) k = -k;
+        tau = -k;
+        m *= s2;
+        x ^= bit;
+        if (kind == 2) z ^= bit;
+      }
+      M[off] = make_float2((float)tau, 0.f);
+    } else if (kind == 3 || kind == 4) {  // absorb the frame into a general dense op
+      const int D = kind == 3 ? 2 : 4;
+      Z P[16];
+      {
+        Z A[4], B[4];
+        const int qa = q0, qb = kind == 4 ? q1 : -1;
+        frame_pauli((x >> qa) & 1, (z >> qa) & 1, A);
+        if (D == 2) {
+          for (int i = 0; i < 4; ++i) P[i] = A[i];
+        } else {
+          frame_pauli((x >> qb) & 1, (z >> qb) & 1, B);
+          for (int i = 0; i < 4; ++i)
+            for (int j = 0; j < 4; ++j) P[i * 4 + j] = zmul(A[(i >> 1) * 2 + (j >> 1)], B[(i & 1) * 2 + (j & 1)]);
+        }
+        x &= ~(1u << qa);
+        z &= ~(1u << qa);
+        if (qb >= 0) {
+          x &= ~(1u << qb);
+          z &= ~(1u << qb);
+        }
+      }
+      Z U[16], N[16];
+      for (int i = 0; i < D * D; ++i) U[i] = {M[off + i].x, M[off + i].y};
+      for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+          Z acc{0, 0};
+          for (int k = 0; k < D; ++k)  // forward: U P ; adjoint: P^dag U = P U (real Pauli products)
+            acc = zadd(acc, adjoint ? zmul(P[i * D + k], U[k * D + j]) : zmul(U[i * D + k], P[k * D + j]));
+          N[i * D + j] = acc;
+        }
+      for (int i = 0; i < D * D; ++i) M[off + i] = make_float2((float)N[i].x, (float)N[i].y);
+    } else if (kind == 5 || kind == 6) {
+      angles[(size_t)row * n_ang + col] = (int32_t)x;
+      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = m;
+    }
+  }
+  if (frame_out) frame_out[row] = QfFrame{x, z, m};
+}
+
 }  // namespace qf
 
 using namespace qf;
@@ -471,8 +588,30 @@ int qf_reduce_slots(const double* partials, int rows, int n_slots, int tiles, co
   const int64_t warps = (int64_t)rows * n_cols;
   const int T = 256;
   reduce_slots_kernel<<<(unsigned)((warps * 32 + T - 1) / T), T, 0, (cudaStream_t)stream>>>(
-      partials, rows, n_slots, tiles, col_ptr, slot_list, n_cols, out, accumulate);
+      partials, rows, n_slots, tiles, col_ptr, slot_list, n_cols, out, accumulate, nullptr);
   return check_launch("reduce_slots_kernel");
+}
+
+int qf_reduce_slots_scaled(const double* partials, int rows, int n_slots, int tiles, const int32_t* col_ptr,
+                           const int32_t* slot_list, int n_cols, double* out, int accumulate,
+                           const double* slot_scale, void* stream) {
+  if (rows == 0 || n_cols == 0) return 0;
+  const int64_t warps = (int64_t)rows * n_cols;
+  const int T = 256;
+  reduce_slots_kernel<<<(unsigned)((warps * 32 + T - 1) / T), T, 0, (cudaStream_t)stream>>>(
+      partials, rows, n_slots, tiles, col_ptr, slot_list, n_cols, out, accumulate, slot_scale);
+  return check_launch("reduce_slots_kernel");
+}
+
+int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, float* mats, int n_mat,
+                  int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
+                  QfFrame* frame_out, void* stream) {
+  if (rows == 0) return 0;
+  const int T = 128;
+  frame_walk_kernel<<<(rows + T - 1) / T, T, 0, (cudaStream_t)stream>>>(
+      events, n_events, adjoint, rows, reinterpret_cast<float2*>(mats), n_mat, angles, n_ang, slot_scale, n_slots,
+      frame_in, frame_out);
+  return check_launch("frame_walk_kernel");
 }
 
 int qf_pauli_expect(const float* psi, int n, int rows, int n_terms, const uint32_t* xmask, const uint32_t* zmask,

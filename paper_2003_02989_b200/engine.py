@@ -8,6 +8,7 @@ is used for device allocation and host<->device copies only.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from dataclasses import dataclass, field
 
@@ -71,6 +72,10 @@ class DeviceProgram:
         self.n_terms = len(r["term_beta"])
         self.tiles = 1 << (prog.n - prog.L)
         self._jit = None
+        self.frame = bool(prog.frame)
+        ev = prog.frame_events if prog.frame_events is not None else np.zeros((0, pl.EV_INTS), np.int32)
+        self.n_events = int(ev.shape[0])
+        self.t_events = up(ev.reshape(-1), torch.int32)
 
     def recipe(self, fixed_t, fixed_rows, const_t, const_rows) -> nat.QfBuildRecipe:
         a = self.r_arrays
@@ -163,7 +168,8 @@ class Bound:
     plan, concrete-gate tables, observable coefficient tables and reduction maps,
     all resident on the device.  ``execute`` then only launches kernels."""
 
-    def __init__(self, engine, circuits, symbol_names, observables, want_grad, device, from_state=False):
+    def __init__(self, engine, circuits, symbol_names, observables, want_grad, device, from_state=False,
+                 want_state=False):
         self.device = device
         self.from_state = from_state
         self.symbol_names = list(symbol_names)
@@ -198,9 +204,17 @@ class Bound:
                     M[k, j] += c
             self.hmix = torch.from_numpy(M).to(device)
             self.lam_diag = bool(self.hkeys) and all(all(p == "Z" for _, p in kk) for kk in self.hkeys)
+        # Pauli-frame normalisation (planner.build_program): only where every output is a
+        # diagonal observable / adjoint gradient and the plan-specialised kernels run
+        from . import jit as _jit
+
+        frame = (os.environ.get("QF_FRAME", "1") not in ("0", "", "false") and not want_state
+                 and bool(obs.diag_ids) and not obs.generic_ids and (not want_grad or self.lam_diag)
+                 and _jit.enabled(len(self.circuits), max(n, pl.N_MIN)))
         self.plan = engine.plan(template, sym_index, obs, want_grad, self.lam_diag,
-                                tuple(self.hkeys) if want_grad else None, device, from_state)
+                                tuple(self.hkeys) if want_grad else None, device, from_state, frame)
         plan = self.plan
+        self.frame = plan.fwd.frame
         fixed_np, const_np = pl.concrete_tables(self.circuits, plan.infos)
         self.fixed_rows, self.const_rows = fixed_np.shape[0], const_np.shape[0]
         self.fixed_t = torch.from_numpy(fixed_np.view(np.float64)).to(device)
@@ -287,6 +301,17 @@ class Bound:
         rec = fw.recipe(self.fixed_t, self.fixed_rows, self.const_t, self.const_rows)
         nat.check(lib.qf_build_ops(C.byref(rec), _ptr(theta), theta.shape[1], B, _ptr(mats), fw.prog.n_mat,
                                    _ptr(angs), fw.prog.n_ang, stream))
+        scale = None
+        if fw.frame:
+            if want_state:
+                raise ValueError("this binding stores frame-normalised states (expectations / gradients "
+                                 "only); bind with want_state=True for states")
+            scale = torch.empty((B, max(fw.prog.n_slots, 1)), dtype=torch.float64, device=dev)
+            frame_f = torch.empty((B, 2), dtype=torch.float64, device=dev)  # QfFrame {u32 x, z; f64 m}
+            nat.check(lib.qf_frame_walk(_ptr(fw.t_events), fw.n_events, 0, B, _ptr(mats), fw.prog.n_mat, _ptr(angs),
+                                        fw.prog.n_ang, _ptr(scale), fw.prog.n_slots, None, _ptr(frame_f), stream))
+        else:
+            frame_f = None
         partials = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
         jf = fw.jit(dev, B)
         if jf is not None:
@@ -300,8 +325,8 @@ class Bound:
             expv = torch.zeros((B, self.n_obs), dtype=torch.float64, device=dev)
             if self.obs.diag_ids:
                 ptr, lst = self.obs_csr
-                nat.check(lib.qf_reduce_slots(_ptr(partials), B, fw.prog.n_slots, fw.tiles, _ptr(ptr), _ptr(lst),
-                                              self.n_obs, _ptr(expv), 0, stream))
+                nat.check(lib.qf_reduce_slots_scaled(_ptr(partials), B, fw.prog.n_slots, fw.tiles, _ptr(ptr),
+                                                     _ptr(lst), self.n_obs, _ptr(expv), 0, _ptr(scale), stream))
             if self.gen_T:
                 xm, zm, ny, cf = self.gen_arrays
                 chunks = ((1 << n_eff) + 2047) // 2048
@@ -317,10 +342,10 @@ class Bound:
             st = psi[:, : (1 << plan.n)]
             out["state"] = st.clone() if want_grad else st
         if want_grad:
-            self._adjoint(lib, psi, theta, upstream, stream, out)
+            self._adjoint(lib, psi, theta, upstream, stream, out, frame_f)
         return out
 
-    def _adjoint(self, lib, psi, theta, upstream, stream, out):
+    def _adjoint(self, lib, psi, theta, upstream, stream, out, frame_f=None):
         plan, dev, B = self.plan, self.device, self.B
         ad = plan.adj
         n_eff = plan.n_eff
@@ -336,6 +361,12 @@ class Bound:
         rec = ad.recipe(self.fixed_a, self.fixed_a_rows, self.const_a, self.const_a_rows)
         nat.check(lib.qf_build_ops(C.byref(rec), _ptr(theta), theta.shape[1], B, _ptr(mats), ad.prog.n_mat,
                                    _ptr(angs), ad.prog.n_ang, stream))
+        scale = None
+        if ad.frame:
+            scale = torch.empty((B, max(ad.prog.n_slots, 1)), dtype=torch.float64, device=dev)
+            nat.check(lib.qf_frame_walk(_ptr(ad.t_events), ad.n_events, 1, B, _ptr(mats), ad.prog.n_mat, _ptr(angs),
+                                        ad.prog.n_ang, _ptr(scale), ad.prog.n_slots, _ptr(frame_f), None,
+                                        stream))
         lam = torch.empty_like(psi)
         if not self.lam_diag:
             if self.hkeys:
@@ -358,13 +389,13 @@ class Bound:
         grad = torch.zeros((B, max(self.S, 1)), dtype=torch.float64, device=dev)
         if self.S:
             ptr, lst = self.grad_csr
-            nat.check(lib.qf_reduce_slots(_ptr(partials), B, ad.prog.n_slots, ad.tiles, _ptr(ptr), _ptr(lst), self.S,
-                                          _ptr(grad), 0, stream))
+            nat.check(lib.qf_reduce_slots_scaled(_ptr(partials), B, ad.prog.n_slots, ad.tiles, _ptr(ptr), _ptr(lst),
+                                                 self.S, _ptr(grad), 0, _ptr(scale), stream))
         if self.lam_diag:
             energy = torch.empty((B, 1), dtype=torch.float64, device=dev)
             ptr, lst = self.energy_csr
-            nat.check(lib.qf_reduce_slots(_ptr(partials), B, ad.prog.n_slots, ad.tiles, _ptr(ptr), _ptr(lst), 1,
-                                          _ptr(energy), 0, stream))
+            nat.check(lib.qf_reduce_slots_scaled(_ptr(partials), B, ad.prog.n_slots, ad.tiles, _ptr(ptr), _ptr(lst),
+                                                 1, _ptr(energy), 0, _ptr(scale), stream))
             out["energy"] = energy[:, 0]
         out["grad"] = grad[:, : self.S]
 
@@ -377,9 +408,9 @@ class Engine:
         self._lock = threading.Lock()
 
     def plan(self, template, symbol_index, obs: ObsInfo, adjoint: bool, lam_diag: bool, hkeys, device,
-             from_state: bool = False):
+             from_state: bool = False, frame: bool = False):
         topo = pl.topology_key(template, symbol_index)
-        key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state)
+        key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state, frame)
         with self._lock:
             hit = self._plans.get(key)
         if hit is not None:
@@ -387,18 +418,21 @@ class Engine:
         n = template.num_qubits
         n_eff = max(n, pl.N_MIN)
         infos = pl.analyse(template, symbol_index)
+        if frame and adjoint:  # forward and adjoint must agree on the stored representation
+            frame = pl.frame_eligible(pl.build_ops(pl.analyse(template, symbol_index), True), infos, True)
         diag_sums = [None] * len(obs.sums)
         for k in obs.diag_ids:
             diag_sums[k] = _TermList(obs.sums[k])
         fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
-                               obs_diag_ids=obs.diag_ids, from_state=from_state)
+                               obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame)
         plan = Plan(n, n_eff, len(symbol_index), infos, DeviceProgram(fwd, device), None, lam_diag, obs)
         plan.extra["from_state"] = from_state
         if adjoint:
             infos_a = pl.analyse(template, symbol_index)
             hterms = _TermList([_Term(dict(kk), 1.0) for kk in hkeys])
             adjp = pl.build_program(template, infos_a, n_eff, adjoint=True, observables=[hterms],
-                                    lam_diag=lam_diag)
+                                    lam_diag=lam_diag, frame=frame)
+            assert adjp.frame == fwd.frame
             plan.adj = DeviceProgram(adjp, device)
             plan.extra["adj_infos"] = infos_a
         with self._lock:
@@ -406,17 +440,17 @@ class Engine:
         return plan
 
     def bind(self, circuits, symbol_names, observables=(), *, want_grad=False, device=None,
-             from_state=False) -> Bound:
+             from_state=False, want_state=False) -> Bound:
         dev = _require_cuda(device)
         symbol_names = tuple(s.name if hasattr(s, "name") else s for s in symbol_names)
         observables = list(observables)
         key = (tuple(map(id, circuits)), symbol_names, tuple(map(id, observables)), bool(want_grad), str(dev),
-               bool(from_state))
+               bool(from_state), bool(want_state))
         with self._lock:
             hit = self._bound.get(key)
         if hit is not None and all(a is b for a, b in zip(hit.circuits, circuits)):
             return hit
-        b = Bound(self, circuits, symbol_names, observables, want_grad, dev, from_state)
+        b = Bound(self, circuits, symbol_names, observables, want_grad, dev, from_state, want_state)
         b._keepalive = observables
         with self._lock:
             if len(self._bound) >= self._max_bound:
@@ -438,7 +472,8 @@ class Engine:
             raise ValueError(f"{len(circuits)} circuits for {B} parameter rows")
         if B == 0:
             return {}
-        bound = self.bind(circuits, symbol_names, observables, want_grad=want_grad, device=dev)
+        bound = self.bind(circuits, symbol_names, observables, want_grad=want_grad, device=dev,
+                          want_state=want_state)
         theta = vals.to(device=dev, dtype=torch.float32).contiguous()
         out = bound.execute(theta, upstream=upstream, want_state=want_state, want_grad=want_grad)
         out["plan"] = bound.plan

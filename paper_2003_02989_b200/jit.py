@@ -218,7 +218,18 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                 s0, s1, moff = int(op[1]), int(op[2]), int(op[3]) - mb
                 slot = int(op[7])
                 cls, gk = int(op[9]), int(op[10])
-                if kind == pl.OP_DENSE1:
+                if kind == pl.OP_DENSE1 and cls in (pl.CLS_NX, pl.CLS_NY):
+                    # Pauli-frame normalised rotation: the build step wrote tau (adjoint-ready)
+                    ax = 1 if cls == pl.CLS_NX else 2
+                    w(f"    {{ const float tau = M[{moff}].x;")
+                    if adj and slot >= 0:
+                        g0 = int(op[8])
+                        sc = float(gm[g0 + 4, 0])
+                        w(f"      GS[{(slot - slb) * NT} + t] = {_flit(sc)} * gradp<{s0}, {NR}, {gk}>(v0, v1);")
+                    if adj:
+                        w(f"      applyN<{s0}, {NR}, {ax}>(v1, tau);")
+                    w(f"      applyN<{s0}, {NR}, {ax}>(v0, tau); }}")
+                elif kind == pl.OP_DENSE1:
                     w(f"    {{ float2 u00 = M[{moff}], u01 = M[{moff + 1}], u10 = M[{moff + 2}], u11 = M[{moff + 3}];")
                     if adj:
                         if slot >= 0:
@@ -256,6 +267,11 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                         groups.setdefault(S, []).append(kk)
                     pre = f"d{k}"
                     w("    {")
+                    xcol = int(op[11])
+                    gv = "gt"
+                    if xcol >= 0:   # Pauli frame: evaluate at index ^ x
+                        gv = f"{pre}gx"
+                        w(f"      const u32 {gv} = gt ^ (u32)ANG[{xcol - ab}];")
                     if kind == pl.OP_DIAG:
                         if adj and slot >= 0:
                             # gradient: sum_S W[S] * B[S], W = WHT(Im(conj(lam) psi)), B[S] = sum w_k sign_k
@@ -272,7 +288,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                                     if wt == 0.0:
                                         continue
                                     m = int(prog.term_mask[kk])
-                                    w(f"      {acc} += (__popc(gt & {m}u) & 1) ? {_flit(-wt)} : {_flit(wt)};")
+                                    w(f"      {acc} += (__popc({gv} & {m}u) & 1) ? {_flit(-wt)} : {_flit(wt)};")
                                 terms_acc.append(f"{pre}W{S} * {acc}")
                             w(f"      GS[{(slot - slb) * NT} + t] = {' + '.join(terms_acc) or '0.f'};")
                         for S, ks in groups.items():
@@ -280,7 +296,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                             for kk in ks:
                                 m = int(prog.term_mask[kk])
                                 col = int(prog.term_idx[kk]) - ab
-                                w(f"      {{ const u32 x = (u32)ANG[{col}]; {pre}a{S} += (__popc(gt & {m}u) & 1) ? (0u - x) : x; }}")
+                                w(f"      {{ const u32 x = (u32)ANG[{col}]; {pre}a{S} += (__popc({gv} & {m}u) & 1) ? (0u - x) : x; }}")
                         o.extend(_wht_code({S: f"{pre}a{S}" for S in groups}, R, "u32", f"{pre}A", "      "))
                         for r in range(NR):
                             w(f"      {{ const float2 ph = phase_turns((int){pre}A{r}, {'true' if adj else 'false'});"
@@ -291,7 +307,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                             for kk in ks:
                                 m = int(prog.term_mask[kk])
                                 col = -1 - int(prog.term_idx[kk]) - cb
-                                w(f"      {{ const float x = CO[{col}]; {pre}a{S} += (__popc(gt & {m}u) & 1) ? -x : x; }}")
+                                w(f"      {{ const float x = CO[{col}]; {pre}a{S} += (__popc({gv} & {m}u) & 1) ? -x : x; }}")
                         o.extend(_wht_code({S: f"{pre}a{S}" for S in groups}, R, "float", f"{pre}A", "      "))
                         w("      float e = 0.f;")
                         for r in range(NR):

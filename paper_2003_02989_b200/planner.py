@@ -50,6 +50,9 @@ def geometry(adjoint: bool) -> tuple:
 
 OP_DENSE1, OP_DENSE2, OP_DIAG, OP_OBS = 1, 2, 3, 4
 CLS_GENERAL, CLS_XLIKE, CLS_REAL = 0, 1, 2   # dense 1q matrix structure classes
+CLS_NX, CLS_NY = 3, 4                       # Pauli-frame normalised X / Y rotations: [[1, -i tau], [-i tau, 1]] / [[1, -tau], [tau, 1]]
+EV_NX, EV_NY, EV_ABS1, EV_ABS2, EV_DIAG, EV_OBS = 1, 2, 3, 4, 5, 6   # frame-walk events
+EV_INTS = 8
 GK_MATRIX, GK_X, GK_Y, GK_Z = 0, 1, 2, 3     # adjoint generator kinds
 INIT_LOAD, INIT_ZERO, INIT_PRODUCT, INIT_LOAD_PSI = 0, 1, 2, 3
 
@@ -80,6 +83,7 @@ class GateInfo:
     fixed: int = -1        # index in the fixed-matrix table (concrete dense gates)
     const_col: int = -1    # first constant-angle column (concrete diagonal gates)
     cls: int = CLS_GENERAL  # dense 1q structure class (same for every row of a topology)
+    axis: str = ""          # "X" / "Y": a 1q rotation exp(-i v P) (+ global phase) -> frame-normalisable
 
 
 def _is_z_only(terms) -> bool:
@@ -98,6 +102,17 @@ def _symbolic_class(terms, targets) -> int:
     if has_ident or len(letters) != 1:
         return CLS_GENERAL
     return {"X": CLS_XLIKE, "Y": CLS_REAL}.get(letters.pop(), CLS_GENERAL)
+
+
+def _rotation_axis(terms, targets) -> str:
+    """"X"/"Y" when the generator is a single-qubit Pauli (plus an identity term)."""
+    if len(targets) != 1:
+        return ""
+    letters = {p for f, c in terms for p in f.values() if c != 0.0}
+    if any(len(f) > 1 for f, _ in terms) or len(letters) != 1:
+        return ""
+    a = letters.pop()
+    return a if a in ("X", "Y") else ""
 
 
 def _matrix_class(m) -> int:
@@ -124,7 +139,8 @@ def topology_key(circuit, symbol_index) -> tuple:
             out.append(("s", tuple(g.targets), symbol_index[e.symbol], e.coeff, e.const, gen))
         else:
             d = _concrete_is_diag(g)
-            out.append(("c", tuple(g.targets), d, CLS_GENERAL if d else _concrete_class(g)))
+            ax = "" if (d or g.matrix is not None) else _rotation_axis(_gate_terms(g), tuple(g.targets))
+            out.append(("c", tuple(g.targets), d, CLS_GENERAL if d else _concrete_class(g), ax))
     return tuple(out)
 
 
@@ -152,10 +168,12 @@ def analyse(circuit, symbol_index) -> list[GateInfo]:
         if e is not None and e.symbol is not None:
             terms = _gate_terms(g)
             infos.append(GateInfo(i, tg, True, _is_z_only(terms), symbol_index[e.symbol],
-                                  float(e.coeff), float(e.const), terms, cls=_symbolic_class(terms, tg)))
+                                  float(e.coeff), float(e.const), terms, cls=_symbolic_class(terms, tg),
+                                  axis=_rotation_axis(terms, tg)))
         else:
             d = _concrete_is_diag(g)
-            infos.append(GateInfo(i, tg, False, d, cls=CLS_GENERAL if d else _concrete_class(g)))
+            ax = "" if (d or g.matrix is not None) else _rotation_axis(_gate_terms(g), tg)
+            infos.append(GateInfo(i, tg, False, d, cls=CLS_GENERAL if d else _concrete_class(g), axis=ax))
     return infos
 
 
@@ -510,6 +528,8 @@ class Program:
     obs_slots: dict               # observable id -> [slots]
     energy_slots: list
     stats: dict
+    frame: bool = False
+    frame_events: np.ndarray = None   # [E, EV_INTS] int32, execution order
 
 
 def _bit_subset(mask: int, reg_glob: list) -> int:
@@ -630,16 +650,36 @@ def _walsh_angles(diag_entries: np.ndarray) -> np.ndarray:
     return a / d
 
 
+def frame_eligible(ops: list[Op], infos, adjoint: bool) -> bool:
+    """Pauli-frame normalisation needs every gradient-carrying dense op to be a single-qubit
+    X/Y rotation (its generator then only changes sign under the frame)."""
+    if not adjoint:
+        return True
+    for op in ops:
+        if op.kind in (OP_DENSE1, OP_DENSE2) and op.symbolic:
+            if op.kind != OP_DENSE1 or any(infos[gi].axis not in ("X", "Y") for gi in op.factors):
+                return False
+    return True
+
+
 def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool,
                   observables=None, obs_diag_ids=(), lam_diag: bool = False,
-                  from_state: bool = False) -> Program:
+                  from_state: bool = False, frame: bool = False) -> Program:
     """Plan + emit.  ``observables``: list of PauliSums; ``obs_diag_ids``: those fused as
     OBS ops at the end of the forward program; ``lam_diag``: adjoint with a diagonal H
     whose lambda-init / energy is fused into the first backward pass; ``from_state``:
-    the forward program starts from a caller-provided state instead of |0...0>."""
+    the forward program starts from a caller-provided state instead of |0...0>.
+
+    ``frame``: Pauli-frame normalisation (see csrc/qf_capi.cu frame_walk_kernel).  Single-
+    qubit X/Y rotations c I - i s P are applied as I - i tau P (|tau| <= 1, one FFMA2 per
+    amplitude); the stored state is psi = sqrt(m) X^x Z^z psi_stored up to a global phase,
+    and the per-row frame (x, z, m) is tracked by the build step in execution order:
+    general dense ops absorb the frame into their matrix, diagonal ops / observables are
+    evaluated at index ^ x, and slot sums are scaled by m (and the generator's sign)."""
     L, R = geometry(adjoint)
     L = min(L, n)
     ops = build_ops(infos, adjoint)
+    frame = frame and frame_eligible(ops, infos, adjoint)
     if from_state and not adjoint:
         init = {}
     else:
@@ -658,6 +698,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         obs_ops = [Op(OP_OBS, tuple(range(n)), obs=0)]
 
     em = Emitter(n, L, R, infos, adjoint)
+    events = []
     # -- generator / fixed tables for the build recipe
     gen_rows = []
     n_fixed = 0
@@ -721,6 +762,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                 orow[0] = op.kind
                 orow[7] = -1
                 orow[8] = -1
+                orow[11] = -1
                 if op.kind in (OP_DENSE1, OP_DENSE2):
                     if op.kind == OP_DENSE1:
                         order = (op.qubits[0],)
@@ -733,6 +775,16 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                     if op.kind == OP_DENSE1:
                         cl = {infos[gi].cls for gi in op.factors}
                         orow[9] = cl.pop() if len(cl) == 1 else CLS_GENERAL
+                        axes = {infos[gi].axis for gi in op.factors}
+                        if frame and len(axes) == 1 and axes <= {"X", "Y"}:
+                            orow[9] = CLS_NX if axes == {"X"} else CLS_NY
+                    ev = None
+                    if frame:
+                        if op.kind == OP_DENSE1:
+                            kind = {CLS_NX: EV_NX, CLS_NY: EV_NY}.get(int(orow[9]), EV_ABS1)
+                            ev = [kind, order[0], -1, int(orow[3]), -1, -1, 0, 0]
+                        else:
+                            ev = [EV_ABS2, order[0], order[1], int(orow[3]), -1, -1, 0, 0]
                     if adjoint and op.symbolic:
                         (gi,) = op.factors
                         info = infos[gi]
@@ -746,6 +798,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                             em.genmats.extend([2.0 * info.coeff * beta, 0.0])
                         orow[7] = em.new_slot()
                         em.grad_slots.setdefault(info.sym, []).append(int(orow[7]))
+                    if ev is not None:
+                        ev[4] = int(orow[7])
+                        events.append(ev)
                 elif op.kind == OP_DIAG:
                     terms = em.diag_terms(op)
                     b_, e_, g_ = em.emit_terms(terms, reg_glob)
@@ -753,6 +808,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                     if adjoint and op.symbolic:
                         orow[7] = em.new_slot()
                         em.grad_slots.setdefault(op.sym, []).append(int(orow[7]))
+                    if frame:
+                        orow[11] = em.angle_col(2, 0, 0.0)
+                        events.append([EV_DIAG, -1, -1, -1, int(orow[7]), int(orow[11]), 0, 0])
                 elif op.kind == OP_OBS:
                     obs = observables[op.obs]
                     terms = []
@@ -769,6 +827,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         em.energy_slots.append(int(orow[7]))
                     else:
                         em.obs_slots.setdefault(op.obs, []).append(int(orow[7]))
+                    if frame:
+                        orow[11] = em.angle_col(2, 0, 0.0)
+                        events.append([EV_OBS, -1, -1, -1, int(orow[7]), int(orow[11]), 0, 0])
                 em.op_rows.append(orow)
             srow[49] = len(em.op_rows)
             em.stage_rows.append(srow)
@@ -832,7 +893,8 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         genmats=np.array(em.genmats, dtype=np.float32),
         n_slots=em.n_slots, n_mat=em.n_mat, n_ang=em.n_ang, n_coef=em.n_coef,
         recipe=recipe, grad_slots=em.grad_slots, obs_slots=em.obs_slots,
-        energy_slots=em.energy_slots, stats=stats,
+        energy_slots=em.energy_slots, stats=stats, frame=frame,
+        frame_events=np.array(events, dtype=np.int32).reshape(-1, EV_INTS),
     )
 
 

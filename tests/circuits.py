@@ -61,3 +61,34 @@ def random_observable(rng, n, diag=False, k=4, identity=True):
         terms.append(PauliString(float(rng.uniform(-2, 2)),
                                  {int(q): ("Z" if diag else "XYZ"[rng.integers(3)]) for q in qs}))
     return PauliSum(terms)
+
+
+def rotation_circuit(rng, n, depth, n_sym):
+    """Symbolic gates are single-qubit rotations only (Pauli-frame eligible adjoint); fixed
+    gates of every kind (Paulis, H/S/T, CZ/CNOT/SWAP, random 1q/2q unitaries, cnot_pow)."""
+    names = [f"s{i}" for i in range(n_sym)]
+    gs = []
+    for _ in range(depth):
+        r = rng.random()
+        if n >= 2 and r < 0.25:
+            a, b = (int(q) for q in rng.choice(n, 2, replace=False))
+            k = rng.random()
+            if k < 0.2:
+                gs.append(Gate((a, b), matrix=random_unitary(4, rng)))
+            elif k < 0.35:
+                gs.append(G.cnot_pow(float(rng.uniform(-1.5, 1.5)), a, b))
+            else:
+                gs.append(F2[rng.integers(3)](a, b))
+        else:
+            q = int(rng.integers(n))
+            k = rng.random()
+            if k < 0.15:
+                gs.append(F1[rng.integers(6)](q))
+            elif k < 0.2:
+                gs.append(Gate((q,), matrix=random_unitary(2, rng)))
+            elif k < 0.35:
+                gs.append(P1[rng.integers(6)](float(rng.uniform(-3, 3)), q))
+            else:
+                gs.append(P1[rng.integers(6)](ParamExpr(names[rng.integers(n_sym)], float(rng.uniform(-1.5, 1.5)),
+                                                        float(rng.uniform(-.5, .5))), q))
+    return Circuit(n, gs)

@@ -36,15 +36,17 @@ def test_struct_layouts_match_ctypes(tmp_path):
     from paper_2003_02989_b200 import _native
 
     src = tmp_path / "sz.c"
-    src.write_text('#include <stdio.h>\n#include "qfb200.h"\nint main(){printf("%zu %zu %zu %zu %zu\\n",'
-                   'sizeof(QfProgram),sizeof(QfBuildRecipe),sizeof(QfPass),sizeof(QfStage),sizeof(QfOp));}')
+    src.write_text('#include <stdio.h>\n#include "qfb200.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu\\n",'
+                   'sizeof(QfProgram),sizeof(QfBuildRecipe),sizeof(QfPass),sizeof(QfStage),sizeof(QfOp),'
+                   'sizeof(QfFrame));}')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     from paper_2003_02989_b200 import planner as pl
 
     assert got == [ctypes.sizeof(_native.QfProgram), ctypes.sizeof(_native.QfBuildRecipe),
-                   4 * pl.PASS_INTS, 4 * pl.STAGE_INTS, 4 * pl.OP_INTS]
+                   4 * pl.PASS_INTS, 4 * pl.STAGE_INTS, 4 * pl.OP_INTS, ctypes.sizeof(_native.QfFrame)]
+    assert ctypes.sizeof(_native.QfFrame) == 16  # engine allocates frames as [rows, 2] float64
 
 
 def test_shard_rows_partition():

@@ -338,3 +338,36 @@ def test_plan_specialised_kernels_match_interpreter(cuda, monkeypatch):
     ee, gg = orc.adjoint_grad(c, obs[0], bind)
     assert out["1"][1][0, 0] == pytest.approx(ee, abs=EXP)
     _close_grad(out["1"][2][0], gg)
+
+
+@pytest.mark.parametrize("seed,n", [(0, 11), (1, 13), (2, 14)])
+def test_pauli_frame_normalised_programs_vs_oracle(cuda, monkeypatch, seed, n):
+    """Plan-specialised kernels with Pauli-frame normalised rotations (engine default for
+    diagonal observables): expectations and adjoint gradients against the oracle, and
+    identical to the same kernels without the frame (QF_FRAME=0)."""
+    from circuits import rotation_circuit
+    from paper_2003_02989_b200.engine import ENGINE
+
+    rng = np.random.default_rng(300 + seed)
+    c = rotation_circuit(rng, n, 220, n_sym=6)
+    syms = circuit_symbols(c)
+    theta = rng.uniform(-3.5, 3.5, size=(4, len(syms))).astype(np.float32)
+    obs = [random_observable(rng, n, diag=True, k=6), random_observable(rng, n, diag=True, k=3)]
+    monkeypatch.setenv("QF_JIT", "1")
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("QF_FRAME", flag)
+        ENGINE._bound.clear()
+        b = ENGINE.bind([c] * 4, syms, obs, want_grad=True)
+        assert b.frame == (flag == "1")
+        out[flag] = ops.expectation_and_gradient([c] * 4, syms, theta, obs, upstream=np.array([[1.0, -0.7]] * 4))
+    np.testing.assert_allclose(out["1"][0], out["0"][0], atol=2e-5)
+    np.testing.assert_allclose(out["1"][1], out["0"][1], atol=5e-5, rtol=1e-5)
+    e_only = ops.expectation([c] * 4, syms, theta, obs)
+    np.testing.assert_allclose(e_only, out["0"][0], atol=2e-5)
+    for b in range(4):
+        bind = dict(zip(syms, theta[b].astype(np.float64)))
+        ref = orc.simulate_amps(c, bind)
+        for k, o in enumerate(obs):
+            assert out["1"][0][b, k] == pytest.approx(orc.expectation(ref, o, n), abs=EXP)
+        _close_grad(out["1"][1][b], orc.adjoint_grad(c, obs[0] + obs[1] * -0.7, bind)[1])

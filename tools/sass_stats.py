@@ -34,11 +34,14 @@ def programs(name):
     obs = analyse_observables([cost])
     infos = pl.analyse(circ, si)
     n = circ.num_qubits
-    fwd = pl.build_program(circ, infos, n, adjoint=False, observables=[_TermList(obs.sums[0])], obs_diag_ids=[0])
+    frame = os.environ.get("QF_FRAME", "1") != "0"
+    fwd = pl.build_program(circ, infos, n, adjoint=False, observables=[_TermList(obs.sums[0])], obs_diag_ids=[0],
+                           frame=frame)
     hk = [tuple(sorted(t.factors.items())) for t in obs.sums[0]]
     lam_diag = all(all(p == "Z" for _, p in k) for k in hk)
     adj = pl.build_program(circ, pl.analyse(circ, si), n, adjoint=True,
-                           observables=[_TermList([_Term(dict(k), 1.0) for k in hk])], lam_diag=lam_diag)
+                           observables=[_TermList([_Term(dict(k), 1.0) for k in hk])], lam_diag=lam_diag,
+                           frame=frame)
     return fwd, adj
 
 
