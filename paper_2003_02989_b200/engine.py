@@ -129,7 +129,9 @@ class ObsInfo:
     key: tuple = ()
 
 
-def analyse_observables(observables) -> ObsInfo:
+def analyse_observables(observables, keep_identity: bool = False) -> ObsInfo:
+    """``keep_identity``: identity terms stay in the (diagonal) observable and are weighted by
+    the state norm -- used for shards of a distributed state, whose norms are not 1."""
     sums = [as_pauli_sum(o) for o in observables]
     ident = np.zeros(len(sums))
     stripped = []
@@ -137,7 +139,7 @@ def analyse_observables(observables) -> ObsInfo:
     for k, s in enumerate(sums):
         terms = []
         for t in s.terms:
-            if not t.factors:
+            if not t.factors and not keep_identity:
                 ident[k] += t.coefficient
             else:
                 terms.append(t)
@@ -169,7 +171,7 @@ class Bound:
     all resident on the device.  ``execute`` then only launches kernels."""
 
     def __init__(self, engine, circuits, symbol_names, observables, want_grad, device, from_state=False,
-                 want_state=False):
+                 want_state=False, norm_identity=False):
         self.device = device
         self.from_state = from_state
         self.symbol_names = list(symbol_names)
@@ -185,7 +187,7 @@ class Bound:
         n = template.num_qubits
         if n > 32:
             raise MemoryError(f"{n} qubits exceeds the engine limit of 32 per device")
-        self.obs = obs = analyse_observables(observables)
+        self.obs = obs = analyse_observables(observables, keep_identity=norm_identity)
         self.n_obs = len(obs.sums)
         self.S = len(self.symbol_names)
         self.want_grad = want_grad
@@ -211,10 +213,13 @@ class Bound:
         frame = (os.environ.get("QF_FRAME", "1") not in ("0", "", "false") and not want_state
                  and bool(obs.diag_ids) and not obs.generic_ids and (not want_grad or self.lam_diag)
                  and _jit.enabled(len(self.circuits), max(n, pl.N_MIN)))
+        over = pl.batch_overrides(template, self.circuits, sym_index, pl.analyse(template, sym_index)) \
+            if len(self.circuits) > 1 else {}
         self.plan = engine.plan(template, sym_index, obs, want_grad, self.lam_diag,
-                                tuple(self.hkeys) if want_grad else None, device, from_state, frame)
+                                tuple(self.hkeys) if want_grad else None, device, from_state, frame, over)
         plan = self.plan
         self.frame = plan.fwd.frame
+
         fixed_np, const_np = pl.concrete_tables(self.circuits, plan.infos)
         self.fixed_rows, self.const_rows = fixed_np.shape[0], const_np.shape[0]
         self.fixed_t = torch.from_numpy(fixed_np.view(np.float64)).to(device)
@@ -270,9 +275,10 @@ class Bound:
         return len(self.circuits)
 
     def execute(self, theta: torch.Tensor, *, upstream=None, want_state=False, want_grad=False,
-                want_expect=True, stream=None, initial=None) -> dict:
+                want_expect=True, stream=None, initial=None, donate=False) -> dict:
         """theta: device float32 [B, S]; initial: [B, 2^n] complex state when bound
-        ``from_state`` (the circuit is applied to it instead of |0...0>).  Returns device tensors."""
+        ``from_state`` (the circuit is applied to it instead of |0...0>; ``donate``: the
+        caller's contiguous complex64 device tensor is updated in place).  Returns device tensors."""
         lib = nat.load()
         dev = self.device
         plan = self.plan
@@ -290,7 +296,9 @@ class Bound:
             if init.shape[1] != (1 << plan.n):
                 raise ValueError(f"initial state has {init.shape[1]} amplitudes, expected {1 << plan.n}")
             if n_eff == plan.n:
-                psi = init.clone()  # kernels update psi in place; never alias the caller's tensor
+                donated = donate and isinstance(initial, torch.Tensor) and initial.is_contiguous() and \
+                    initial.dtype == torch.complex64 and initial.device == dev
+                psi = init if donated else init.clone()  # kernels update psi in place
             else:
                 psi = torch.zeros((B, 1 << n_eff), dtype=torch.complex64, device=dev)
                 psi[:, : 1 << plan.n] = init
@@ -408,18 +416,20 @@ class Engine:
         self._lock = threading.Lock()
 
     def plan(self, template, symbol_index, obs: ObsInfo, adjoint: bool, lam_diag: bool, hkeys, device,
-             from_state: bool = False, frame: bool = False):
+             from_state: bool = False, frame: bool = False, overrides=None):
+        overrides = overrides or {}
         topo = pl.topology_key(template, symbol_index)
-        key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state, frame)
+        key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state, frame,
+               tuple(sorted(overrides.items())))
         with self._lock:
             hit = self._plans.get(key)
         if hit is not None:
             return hit
         n = template.num_qubits
         n_eff = max(n, pl.N_MIN)
-        infos = pl.analyse(template, symbol_index)
+        infos = pl.analyse(template, symbol_index, overrides)
         if frame and adjoint:  # forward and adjoint must agree on the stored representation
-            frame = pl.frame_eligible(pl.build_ops(pl.analyse(template, symbol_index), True), infos, True)
+            frame = pl.frame_eligible(pl.build_ops(pl.analyse(template, symbol_index, overrides), True), infos, True)
         diag_sums = [None] * len(obs.sums)
         for k in obs.diag_ids:
             diag_sums[k] = _TermList(obs.sums[k])
@@ -428,7 +438,7 @@ class Engine:
         plan = Plan(n, n_eff, len(symbol_index), infos, DeviceProgram(fwd, device), None, lam_diag, obs)
         plan.extra["from_state"] = from_state
         if adjoint:
-            infos_a = pl.analyse(template, symbol_index)
+            infos_a = pl.analyse(template, symbol_index, overrides)
             hterms = _TermList([_Term(dict(kk), 1.0) for kk in hkeys])
             adjp = pl.build_program(template, infos_a, n_eff, adjoint=True, observables=[hterms],
                                     lam_diag=lam_diag, frame=frame)
@@ -440,17 +450,18 @@ class Engine:
         return plan
 
     def bind(self, circuits, symbol_names, observables=(), *, want_grad=False, device=None,
-             from_state=False, want_state=False) -> Bound:
+             from_state=False, want_state=False, norm_identity=False) -> Bound:
         dev = _require_cuda(device)
         symbol_names = tuple(s.name if hasattr(s, "name") else s for s in symbol_names)
         observables = list(observables)
         key = (tuple(map(id, circuits)), symbol_names, tuple(map(id, observables)), bool(want_grad), str(dev),
-               bool(from_state), bool(want_state))
+               bool(from_state), bool(want_state), bool(norm_identity))
         with self._lock:
             hit = self._bound.get(key)
         if hit is not None and all(a is b for a, b in zip(hit.circuits, circuits)):
             return hit
-        b = Bound(self, circuits, symbol_names, observables, want_grad, dev, from_state, want_state)
+        b = Bound(self, circuits, symbol_names, observables, want_grad, dev, from_state, want_state,
+                  norm_identity)
         b._keepalive = observables
         with self._lock:
             if len(self._bound) >= self._max_bound:

@@ -43,6 +43,9 @@ class QfJitArgs(C.Structure):
                 ("coef_stride", C.c_int), ("n_slots", C.c_int), ("tiles_log2", C.c_int), ("pad", C.c_int)]
 
 
+GS_THREAD_BYTES = 40 * 1024
+
+
 def _flit(x: float) -> str:
     return repr(float(np.float32(x))) + "f"
 
@@ -109,7 +112,16 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         outer = [int(x) for x in p[16:16 + n_out]]
         init_mat = [int(x) for x in p[48:48 + n]]
         mcnt, acnt, ccnt, scnt = me - mb, ae - ab, ce - cb, sle - slb
-        smem = NA * TILE * 8 + mcnt * 8 + acnt * 4 + ccnt * 4 + scnt * NT * 4 + 16
+        # slot partials: one float per thread and slot, or (many slots) one per warp after a
+        # shuffle reduction, so the CTA keeps its occupancy
+        per_thread_gs = scnt * NT * 4 <= GS_THREAD_BYTES
+        GSW = NT if per_thread_gs else NT // 32
+        smem = NA * TILE * 8 + mcnt * 8 + acnt * 4 + ccnt * 4 + scnt * GSW * 4 + 16
+
+        def gs_store(slot_rel, expr):
+            if per_thread_gs:
+                return f"GS[{slot_rel * NT} + t] = {expr};"
+            return f"{{ const float gsv = warp_sum_f({expr}); if ((t & 31u) == 0u) GS[{slot_rel * GSW} + (t >> 5)] = gsv; }}"
         geo.append((NT, smem))
         o = []
         w = o.append
@@ -158,10 +170,15 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         st0 = st_rows[0]
         w(f"  const u32 gt0 = base | {_xor_expr(tglob(st0))};")
         if init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI):
+            # pointer + 64-bit constant offsets: u32 index sums above 2^29 elements were
+            # miscompiled (half-width loads) by nvcc/NVRTC 12.9 at n >= 30
+            w("  const float2* __restrict__ pt0 = psi + gt0;")
+            if adj and init == pl.INIT_LOAD:
+                w("  const float2* __restrict__ lt0 = lam + gt0;")
             for r in range(NR):
-                w(f"  v0[{r}] = psi[gt0 + {roff(st0, r)}u];")
+                w(f"  v0[{r}] = pt0[{roff(st0, r)}ll];")
                 if adj:
-                    w(f"  v1[{r}] = " + (f"lam[gt0 + {roff(st0, r)}u];" if init == pl.INIT_LOAD else
+                    w(f"  v1[{r}] = " + (f"lt0[{roff(st0, r)}ll];" if init == pl.INIT_LOAD else
                                           "make_float2(0.f, 0.f);"))
         elif init == pl.INIT_ZERO:
             w("  v0[0] = make_float2(gt0 == 0u ? 1.f : 0.f, 0.f);")
@@ -225,7 +242,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                     if adj and slot >= 0:
                         g0 = int(op[8])
                         sc = float(gm[g0 + 4, 0])
-                        w(f"      GS[{(slot - slb) * NT} + t] = {_flit(sc)} * gradp<{s0}, {NR}, {gk}>(v0, v1);")
+                        w("      " + gs_store(slot - slb, f"{_flit(sc)} * gradp<{s0}, {NR}, {gk}>(v0, v1)"))
                     if adj:
                         w(f"      applyN<{s0}, {NR}, {ax}>(v1, tau);")
                     w(f"      applyN<{s0}, {NR}, {ax}>(v0, tau); }}")
@@ -240,7 +257,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                             else:
                                 gl = [f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})" for i in range(4)]
                                 w(f"      const float gacc = grad1<{s0}, {NR}>(v0, v1, {', '.join(gl)});")
-                            w(f"      GS[{(slot - slb) * NT} + t] = gacc;")
+                            w("      " + gs_store(slot - slb, "gacc"))
                         w("      { const float2 x = u01; u00.y = -u00.y; u11.y = -u11.y;"
                           " u01 = make_float2(u10.x, -u10.y); u10 = make_float2(x.x, -x.y); }")
                         w(f"      apply1<{s0}, {NR}, {cls}>(v1, u00, u01, u10, u11);")
@@ -254,7 +271,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                             gl = ", ".join(f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})"
                                            for i in range(16))
                             w(f"      const float2 g[16] = {{{gl}}};")
-                            w(f"      GS[{(slot - slb) * NT} + t] = grad2<{s0}, {s1}, {NR}>(v0, v1, g);")
+                            w("      " + gs_store(slot - slb, f"grad2<{s0}, {s1}, {NR}>(v0, v1, g)"))
                         w(f"      apply2<{s0}, {s1}, {NR}>(v0, m); apply2<{s0}, {s1}, {NR}>(v1, m); }}")
                     else:
                         w(f"    {{ float2 m[16]; for (int i = 0; i < 16; ++i) m[i] = M[{moff} + i];")
@@ -290,7 +307,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                                     m = int(prog.term_mask[kk])
                                     w(f"      {acc} += (__popc({gv} & {m}u) & 1) ? {_flit(-wt)} : {_flit(wt)};")
                                 terms_acc.append(f"{pre}W{S} * {acc}")
-                            w(f"      GS[{(slot - slb) * NT} + t] = {' + '.join(terms_acc) or '0.f'};")
+                            w("      " + gs_store(slot - slb, " + ".join(terms_acc) or "0.f"))
                         for S, ks in groups.items():
                             w(f"      u32 {pre}a{S} = 0u;")
                             for kk in ks:
@@ -315,7 +332,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                             if adj:
                                 w(f"      v1[{r}] = cscale({pre}A{r}, v0[{r}]);")
                         if slot >= 0:
-                            w(f"      GS[{(slot - slb) * NT} + t] = e;")
+                            w("      " + gs_store(slot - slb, "e"))
                     w("    }")
             w("  }")
 
@@ -323,16 +340,19 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         if store:
             stl = st_rows[-1]
             w(f"  {{ const u32 gs = base | {_xor_expr(tglob(stl))};")
+            w("    float2* __restrict__ pts = psi + gs;")
+            if adj:
+                w("    float2* __restrict__ lts = lam + gs;")
             for r in range(NR):
-                w(f"    psi[gs + {roff(stl, r)}u] = v0[{r}];")
+                w(f"    pts[{roff(stl, r)}ll] = v0[{r}];")
                 if adj:
-                    w(f"    lam[gs + {roff(stl, r)}u] = v1[{r}];")
+                    w(f"    lts[{roff(stl, r)}ll] = v1[{r}];")
             w("  }")
         if scnt:
             w("  __syncthreads();")
             w(f"  for (int s = t >> 5; s < {scnt}; s += {max(NT // 32, 1)}) {{")
             w("    double acc = 0.0;")
-            w(f"    for (int i = (t & 31); i < {NT}; i += 32) acc += (double)GS[s * {NT} + i];")
+            w(f"    for (int i = (t & 31); i < {GSW}; i += 32) acc += (double)GS[s * {GSW} + i];")
             w("    acc = warp_sum_d(acc);")
             w(f"    if ((t & 31) == 0) a.partials[((size_t)row * a.n_slots + {slb} + s) * {1 << (n - L)} + o] = acc;")
             w("  }")

@@ -144,6 +144,62 @@ def topology_key(circuit, symbol_index) -> tuple:
     return tuple(out)
 
 
+def _class_ok(cls: int, m) -> bool:
+    """Does matrix m have the structure the kernels assume for class ``cls``?"""
+    if cls == CLS_GENERAL or m.shape[0] != 2:
+        return True
+    if cls == CLS_REAL:
+        return bool(np.all(m.imag == 0))
+    return bool(m[0, 0].imag == 0 and m[1, 1].imag == 0 and m[0, 1].real == 0 and m[1, 0].real == 0)
+
+
+def batch_overrides(template, circuits, symbol_index, infos) -> dict:
+    """Rows of one plan must share the template's gate structure (targets, symbols,
+    generators, diagonal-ness); concrete values may differ.  Returns {gate index: (cls,
+    axis)} where some row's matrix does not fit the template's class / rotation axis (the
+    plan then uses the general form for that gate).  Raises ValueError on structure."""
+    over: dict = {}
+    seen = {id(template)}
+    for c in circuits:
+        if id(c) in seen:
+            continue
+        seen.add(id(c))
+        if c.num_qubits != template.num_qubits or len(c.gates) != len(template.gates):
+            raise ValueError("all circuits of a batch must share one gate structure")
+        for i, (gc, gt) in enumerate(zip(c.gates, template.gates)):
+            if gc is gt:
+                continue
+            info = infos[i]
+            bad = tuple(int(q) for q in gc.targets) != info.targets
+            ec = gc.exponent
+            sym = ec is not None and ec.symbol is not None
+            if not bad and sym != info.symbolic:
+                bad = True
+            if not bad and sym:
+                et = gt.exponent
+                bad = (symbol_index.get(ec.symbol) != info.sym or ec.coeff != et.coeff or ec.const != et.const
+                       or (gc.generator is not gt.generator and
+                           sorted(((tuple(sorted(t.factors.items())), t.coefficient) for t in gc.generator.terms))
+                           != sorted(((tuple(sorted(t.factors.items())), t.coefficient) for t in gt.generator.terms))))
+            elif not bad:
+                m = concrete_matrix(gc)
+                if info.diag:
+                    bad = not bool(np.all(m[~np.eye(m.shape[0], dtype=bool)] == 0))
+                else:
+                    cls, ax = over.get(i, (info.cls, info.axis))
+                    if not _class_ok(cls, m):
+                        cls = CLS_GENERAL
+                    if ax and (gc.matrix is not None or _rotation_axis(_gate_terms(gc), info.targets) != ax):
+                        ax = ""
+                    if (cls, ax) != (info.cls, info.axis):
+                        over[i] = (cls, ax)
+            if bad:
+                raise ValueError(f"gate {i} of a batch row differs in structure from the first row's "
+                                 "(targets, generator, symbol, diagonal-ness); rows of one call must share "
+                                 "a topology")
+    return over
+
+
 _DIAG_CACHE: dict = {}
 
 
@@ -160,7 +216,8 @@ def _concrete_is_diag(g) -> bool:
     return d
 
 
-def analyse(circuit, symbol_index) -> list[GateInfo]:
+def analyse(circuit, symbol_index, overrides=None) -> list[GateInfo]:
+    """``overrides``: {gate index: (cls, axis)} from batch_overrides."""
     infos = []
     for i, g in enumerate(circuit.gates):
         e = g.exponent
@@ -173,7 +230,10 @@ def analyse(circuit, symbol_index) -> list[GateInfo]:
         else:
             d = _concrete_is_diag(g)
             ax = "" if (d or g.matrix is not None) else _rotation_axis(_gate_terms(g), tg)
-            infos.append(GateInfo(i, tg, False, d, cls=CLS_GENERAL if d else _concrete_class(g), axis=ax))
+            cls = CLS_GENERAL if d else _concrete_class(g)
+            if overrides and i in overrides:
+                cls, ax = overrides[i]
+            infos.append(GateInfo(i, tg, False, d, cls=cls, axis=ax))
     return infos
 
 

@@ -119,7 +119,36 @@ def cfg5(steps):
     th = torch.zeros((1, 0), device="cuda")
     b = ENGINE.bind([circ], [], obs)
     ms = timed(lambda: b.execute(th), max(1, steps // 2), warmup=1)
-    report("cfg5_brickwork32_d14_expectation_1gpu", 1, ms, b, False)
+    e = float(b.execute(th)["expectations"][0, 0])
+    report("cfg5_brickwork32_d14_expectation_1gpu", 1, ms, b, False, {"expectation": e})
+
+
+def cfg5_sharded(steps):
+    """The cfg-5 sharded schedule (2/4/8 shards) emulated on one GPU: every shard's tile
+    passes run here and the all-to-all is a device transpose (LoopbackExchange)."""
+    from paper_2003_02989_b200 import distributed as D
+
+    circ = wl.brickwork_circuit(32, 14, wl.SEED_BIG)
+    obs = wl.z_sum(32)
+    for g in (1, 2, 3):
+        marks = []
+
+        def timer(kind, k):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            marks.append((kind, ev))
+
+        e, plan = D.run_sharded(circ, obs, g, D.LoopbackExchange(g))   # warm-up (plans, JIT)
+        torch.cuda.synchronize()
+        marks.clear()
+        t0 = time.perf_counter()
+        e, plan = D.run_sharded(circ, obs, g, D.LoopbackExchange(g), timer=timer)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        parts = [(marks[i][0], round(marks[i][1].elapsed_time(marks[i + 1][1]), 2)) for i in range(len(marks) - 1)]
+        print(json.dumps({"config": f"cfg5_brickwork32_d14_sharded_g{g}_loopback_1gpu", "expectation": e,
+                          "swaps": plan.swaps, "wall_s": round(wall, 3), "step_ms": parts}), flush=True)
+        torch.cuda.empty_cache()
 
 
 def main():
