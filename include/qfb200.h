@@ -21,6 +21,10 @@
  *   qf_pauli_expect   pauli_term_values + expectation  qcflow/sim.py:177-213
  *   qf_pauli_apply    (H|psi>, adjoint seed)        index/phase form of qcflow/sim.py:183-196
  *   qf_sample         _draw_bits / sample            qcflow/sim.py:216-227, rng.py:14-19
+ *   qf_frame_walk     per-row Pauli-frame re-factorisation of the gate_matrix products
+ *                                                   qcflow/circuit.py:281-309 (exact, see planner.py)
+ *   qf_reduce_slots_scaled  _pairwise_sum with per-row frame scales  qcflow/sim.py:162-174
+ *   qf_jit_*          compile / load / launch the plan-specialised pass kernels (jit.py)
  */
 #ifndef QFB200_H
 #define QFB200_H

@@ -95,7 +95,8 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
     NR, NT = 1 << R, 1 << TB
     NA = 2 if adj else 1
     TILE = 1 << L
-    minb = int(os.environ.get("QF_MINB_ADJ" if adj else "QF_MINB_FWD", "0")) or max(1, min(8, 65536 // (NT * (NR * 2 * NA + 32))))
+    env_minb = int(os.environ.get("QF_MINB_ADJ" if adj else "QF_MINB_FWD", "0"))
+    minb = env_minb or max(1, min(8, 65536 // (NT * (NR * 2 * NA + 32))))
     gm = prog.genmats.reshape(-1, 2) if len(prog.genmats) else np.zeros((0, 2), np.float32)
     src = []
     names, geo = [], []
@@ -116,7 +117,12 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         # shuffle reduction, so the CTA keeps its occupancy
         per_thread_gs = scnt * NT * 4 <= GS_THREAD_BYTES
         GSW = NT if per_thread_gs else NT // 32
-        smem = NA * TILE * 8 + mcnt * 8 + acnt * 4 + ccnt * 4 + scnt * GSW * 4 + 16
+        smem = NA * TILE * 8 + mcnt * 16 + acnt * 4 + ccnt * 4 + scnt * GSW * 4 + 16
+        pass_ops = [prog.ops[k] for s_ in range(sb, se) for k in range(int(prog.stages[s_][48]),
+                                                                        int(prog.stages[s_][49]))]
+        heavy = any(int(op_[0]) == pl.OP_DENSE2 or (int(op_[0]) == pl.OP_DENSE1 and int(op_[9]) == pl.CLS_GENERAL)
+                    for op_ in pass_ops)
+        minb_p = min(minb, 2) if (heavy and not env_minb) else minb
 
         def gs_store(slot_rel, expr):
             if per_thread_gs:
@@ -125,18 +131,33 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         geo.append((NT, smem))
         o = []
         w = o.append
-        w(f'extern "C" __global__ void __launch_bounds__({NT}, {minb}) {name}(const QfJitArgs a) {{')
+        w(f'extern "C" __global__ void __launch_bounds__({NT}, {minb_p}) {name}(const QfJitArgs a) {{')
         w("  extern __shared__ __align__(16) unsigned char smem_raw[];")
         w("  float2* sm = reinterpret_cast<float2*>(smem_raw);")
         w(f"  float2* M = sm + {NA * TILE};")
-        w(f"  int* ANG = reinterpret_cast<int*>(M + {mcnt});")
+        w(f"  u64* MN = reinterpret_cast<u64*>(M + {mcnt});   // (-Im, Im) pairs of M")
+        w(f"  int* ANG = reinterpret_cast<int*>(MN + {mcnt});")
         w(f"  float* CO = reinterpret_cast<float*>(ANG + {acnt});")
         w(f"  float* GS = CO + {ccnt};")
         w("  const u32 t = threadIdx.x;")
         w(f"  const int row = (int)(blockIdx.x >> {n - L});")
         w(f"  const u32 o = blockIdx.x & {(1 << (n - L)) - 1}u;")
         if mcnt:
-            w(f"  for (int i = t; i < {mcnt}; i += {NT}) M[i] = a.mats[(size_t)row * a.n_mat + {mb} + i];")
+            # stage the row's matrices: as built for the forward sweep; conjugate-transposed
+            # (U^dag) for general / X-like / real dense ops of the adjoint sweep
+            w(f"  {{ const float2* __restrict__ src = a.mats + (size_t)row * a.n_mat + {mb};")
+            w(f"    for (int i = t; i < {mcnt}; i += {NT}) {{ const float2 x = src[i]; M[i] = x; MN[i] = pk_negpos(x.y); }}")
+            if adj:
+                for op_ in pass_ops:
+                    kd, cl_ = int(op_[0]), int(op_[9])
+                    if kd not in (pl.OP_DENSE1, pl.OP_DENSE2) or cl_ in (pl.CLS_NX, pl.CLS_NY):
+                        continue
+                    D = 2 if kd == pl.OP_DENSE1 else 4
+                    off = int(op_[3]) - mb
+                    w(f"    __syncthreads();")
+                    w(f"    if (t < {D * D}) {{ const float2 x = src[{off} + (t % {D}) * {D} + t / {D}];"
+                      f" M[{off} + t] = make_float2(x.x, -x.y); MN[{off} + t] = pk_negpos(-x.y); }}")
+            w("  }")
         if acnt:
             w(f"  for (int i = t; i < {acnt}; i += {NT}) ANG[i] = a.angles[(size_t)row * a.n_ang + {ab} + i];")
         if ccnt:
@@ -247,7 +268,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                         w(f"      applyN<{s0}, {NR}, {ax}>(v1, tau);")
                     w(f"      applyN<{s0}, {NR}, {ax}>(v0, tau); }}")
                 elif kind == pl.OP_DENSE1:
-                    w(f"    {{ float2 u00 = M[{moff}], u01 = M[{moff + 1}], u10 = M[{moff + 2}], u11 = M[{moff + 3}];")
+                    w(f"    {{ const float2 u00 = M[{moff}], u01 = M[{moff + 1}], u10 = M[{moff + 2}], u11 = M[{moff + 3}];")
                     if adj:
                         if slot >= 0:
                             g0 = int(op[8])
@@ -258,24 +279,27 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                                 gl = [f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})" for i in range(4)]
                                 w(f"      const float gacc = grad1<{s0}, {NR}>(v0, v1, {', '.join(gl)});")
                             w("      " + gs_store(slot - slb, "gacc"))
-                        w("      { const float2 x = u01; u00.y = -u00.y; u11.y = -u11.y;"
-                          " u01 = make_float2(u10.x, -u10.y); u10 = make_float2(x.x, -x.y); }")
-                        w(f"      apply1<{s0}, {NR}, {cls}>(v1, u00, u01, u10, u11);")
-                    w(f"      apply1<{s0}, {NR}, {cls}>(v0, u00, u01, u10, u11); }}")
+                        if cls == pl.CLS_GENERAL:
+                            w(f"      apply1m<{s0}, {NR}>(v1, M + {moff}, MN + {moff});")
+                        else:
+                            w(f"      apply1<{s0}, {NR}, {cls}>(v1, u00, u01, u10, u11);")
+                    if cls == pl.CLS_GENERAL:
+                        w(f"      apply1m<{s0}, {NR}>(v0, M + {moff}, MN + {moff}); }}")
+                    else:
+                        w(f"      apply1<{s0}, {NR}, {cls}>(v0, u00, u01, u10, u11); }}")
                 elif kind == pl.OP_DENSE2:
                     if adj:
-                        w(f"    {{ float2 m[16]; for (int i = 0; i < 4; ++i) for (int j = 0; j < 4; ++j) "
-                          f"{{ const float2 x = M[{moff} + j * 4 + i]; m[i * 4 + j] = make_float2(x.x, -x.y); }}")
+                        w("    {")
                         if slot >= 0:
                             g0 = int(op[8])
                             gl = ", ".join(f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})"
                                            for i in range(16))
                             w(f"      const float2 g[16] = {{{gl}}};")
                             w("      " + gs_store(slot - slb, f"grad2<{s0}, {s1}, {NR}>(v0, v1, g)"))
-                        w(f"      apply2<{s0}, {s1}, {NR}>(v0, m); apply2<{s0}, {s1}, {NR}>(v1, m); }}")
+                        w(f"      apply2m<{s0}, {s1}, {NR}>(v0, M + {moff}, MN + {moff});"
+                          f" apply2m<{s0}, {s1}, {NR}>(v1, M + {moff}, MN + {moff}); }}")
                     else:
-                        w(f"    {{ float2 m[16]; for (int i = 0; i < 16; ++i) m[i] = M[{moff} + i];")
-                        w(f"      apply2<{s0}, {s1}, {NR}>(v0, m); }}")
+                        w(f"    apply2m<{s0}, {s1}, {NR}>(v0, M + {moff}, MN + {moff});")
                 elif kind in (pl.OP_DIAG, pl.OP_OBS):
                     tb, te = int(op[4]), int(op[5])
                     groups: dict = {}

@@ -16,4 +16,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > $OUT/ncu_launch.log 2>&1; echo "ncu launches rc=$?" >> $OUT/ncu_launch.log
 QF_B=32 timeout 900 ncu --set full --clock-control none --import-source on -k regex:qf_[af]_p -c 12 \
   -o $OUT/passes python tools/prof_qaoa.py > $OUT/ncu_full.log 2>&1; echo "ncu full rc=$?" >> $OUT/ncu_full.log
+timeout 900 python tools/configs_bench.py --steps 3 > $OUT/configs.jsonl 2>&1
+timeout 600 ncu --set full --clock-control none -k regex:qf_f_p -c 3 -o $OUT/rcs python tools/configs_bench.py cfg4 --steps 1 > $OUT/ncu_rcs.log 2>&1
 ls -la $OUT

@@ -26,7 +26,7 @@ def programs(name):
     elif name == "rcs":
         circ = wl.rcs_circuits(1, 24, 20)[0]
         from paper_2003_02989_b200.pauli import PauliSum, PauliString
-        cost = PauliSum([PauliString({q: "Z"}, 1.0) for q in range(24)])
+        cost = PauliSum([PauliString(1.0, {q: "Z"}) for q in range(24)])
     else:
         raise SystemExit(f"unknown workload {name}")
     syms = circuit_symbols(circ)
