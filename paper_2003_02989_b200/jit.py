@@ -313,14 +313,30 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                     if xcol >= 0:   # Pauli frame: evaluate at index ^ x
                         gv = f"{pre}gx"
                         w(f"      const u32 {gv} = gt ^ (u32)ANG[{xcol - ab}];")
+                    # register slots the phase polynomial depends on: with 2^k < 2^R distinct
+                    # values per thread, evaluate 2^k phases (table) instead of one per amplitude
+                    kbits = sorted({j for S in groups for j in range(R) if S >> j & 1})
+                    table = (1 << len(kbits)) < NR
+
+                    def cidx(r):
+                        return sum(((r >> j) & 1) << i for i, j in enumerate(kbits))
+
+                    def csub(S):
+                        return sum(((S >> j) & 1) << i for i, j in enumerate(kbits))
+
+                    def signed_sum(names_by_S, c, zero):
+                        parts = []
+                        for S, nm in names_by_S.items():
+                            neg = bin(csub(S) & c).count("1") & 1
+                            parts.append(("-" if neg else "+") + nm)
+                        if not parts:
+                            return zero
+                        e = " ".join(parts)
+                        return e[1:] if e[0] == "+" else "(" + zero + " " + e + ")"
+
                     if kind == pl.OP_DIAG:
                         if adj and slot >= 0:
-                            # gradient: sum_S W[S] * B[S], W = WHT(Im(conj(lam) psi)), B[S] = sum w_k sign_k
-                            for r in range(NR):
-                                w(f"      const float {pre}w{r} = im_conj_mul(v1[{r}], v0[{r}]);")
-                            wl = _wht_code({r: f"{pre}w{r}" for r in range(NR)}, R, "float", f"{pre}W", "      ")
-                            o.extend(wl)
-                            terms_acc = []
+                            bnames = {}
                             for S, ks in groups.items():
                                 acc = f"{pre}b{S}"
                                 w(f"      float {acc} = 0.f;")
@@ -330,18 +346,46 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                                         continue
                                     m = int(prog.term_mask[kk])
                                     w(f"      {acc} += (__popc({gv} & {m}u) & 1) ? {_flit(-wt)} : {_flit(wt)};")
-                                terms_acc.append(f"{pre}W{S} * {acc}")
-                            w("      " + gs_store(slot - slb, " + ".join(terms_acc) or "0.f"))
+                                bnames[S] = acc
+                            if table:
+                                # grad = sum_c h[c] * sum_{r: c(r)=c} Im(conj(lam_r) psi_r)
+                                terms_acc = []
+                                for c in range(1 << len(kbits)):
+                                    rs = [r for r in range(NR) if cidx(r) == c]
+                                    w(f"      float {pre}q{c} = 0.f;")
+                                    for r in rs:
+                                        w(f"      {pre}q{c} = fmaf(v1[{r}].x, v0[{r}].y, fmaf(-v1[{r}].y, v0[{r}].x, {pre}q{c}));")
+                                    terms_acc.append(f"({signed_sum(bnames, c, '0.f')}) * {pre}q{c}")
+                                w("      " + gs_store(slot - slb, " + ".join(terms_acc) or "0.f"))
+                            else:
+                                # gradient: sum_S W[S] * B[S], W = WHT(Im(conj(lam) psi)), B[S] = sum w_k sign_k
+                                for r in range(NR):
+                                    w(f"      const float {pre}w{r} = im_conj_mul(v1[{r}], v0[{r}]);")
+                                wl = _wht_code({r: f"{pre}w{r}" for r in range(NR)}, R, "float", f"{pre}W", "      ")
+                                o.extend(wl)
+                                terms_acc = [f"{pre}W{S} * {bnames[S]}" for S in bnames]
+                                w("      " + gs_store(slot - slb, " + ".join(terms_acc) or "0.f"))
                         for S, ks in groups.items():
                             w(f"      u32 {pre}a{S} = 0u;")
                             for kk in ks:
                                 m = int(prog.term_mask[kk])
                                 col = int(prog.term_idx[kk]) - ab
                                 w(f"      {{ const u32 x = (u32)ANG[{col}]; {pre}a{S} += (__popc({gv} & {m}u) & 1) ? (0u - x) : x; }}")
-                        o.extend(_wht_code({S: f"{pre}a{S}" for S in groups}, R, "u32", f"{pre}A", "      "))
-                        for r in range(NR):
-                            w(f"      {{ const float2 ph = phase_turns((int){pre}A{r}, {'true' if adj else 'false'});"
-                              f" v0[{r}] = cmul(v0[{r}], ph);" + (f" v1[{r}] = cmul(v1[{r}], ph);" if adj else "") + " }")
+                        inv = 'true' if adj else 'false'
+                        if table:
+                            anames = {S: f"{pre}a{S}" for S in groups}
+                            for c in range(1 << len(kbits)):
+                                w(f"      const float2 {pre}P{c} = phase_turns((int)({signed_sum(anames, c, '0u')}), {inv});")
+                                w(f"      const u64 {pre}N{c} = pk_negpos({pre}P{c}.y);")
+                            for r in range(NR):
+                                c = cidx(r)
+                                w(f"      v0[{r}] = cmulp(v0[{r}], {pre}P{c}.x, {pre}N{c});" +
+                                  (f" v1[{r}] = cmulp(v1[{r}], {pre}P{c}.x, {pre}N{c});" if adj else ""))
+                        else:
+                            o.extend(_wht_code({S: f"{pre}a{S}" for S in groups}, R, "u32", f"{pre}A", "      "))
+                            for r in range(NR):
+                                w(f"      {{ const float2 ph = phase_turns((int){pre}A{r}, {inv});"
+                                  f" v0[{r}] = cmul(v0[{r}], ph);" + (f" v1[{r}] = cmul(v1[{r}], ph);" if adj else "") + " }")
                     else:  # OBS
                         for S, ks in groups.items():
                             w(f"      float {pre}a{S} = 0.f;")
@@ -349,12 +393,19 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                                 m = int(prog.term_mask[kk])
                                 col = -1 - int(prog.term_idx[kk]) - cb
                                 w(f"      {{ const float x = CO[{col}]; {pre}a{S} += (__popc({gv} & {m}u) & 1) ? -x : x; }}")
-                        o.extend(_wht_code({S: f"{pre}a{S}" for S in groups}, R, "float", f"{pre}A", "      "))
+                        if table:
+                            anames = {S: f"{pre}a{S}" for S in groups}
+                            for c in range(1 << len(kbits)):
+                                w(f"      const float {pre}C{c} = {signed_sum(anames, c, '0.f')};")
+                            coef = {r: f"{pre}C{cidx(r)}" for r in range(NR)}
+                        else:
+                            o.extend(_wht_code({S: f"{pre}a{S}" for S in groups}, R, "float", f"{pre}A", "      "))
+                            coef = {r: f"{pre}A{r}" for r in range(NR)}
                         w("      float e = 0.f;")
                         for r in range(NR):
-                            w(f"      e = fmaf({pre}A{r}, fmaf(v0[{r}].x, v0[{r}].x, v0[{r}].y * v0[{r}].y), e);")
+                            w(f"      e = fmaf({coef[r]}, fmaf(v0[{r}].x, v0[{r}].x, v0[{r}].y * v0[{r}].y), e);")
                             if adj:
-                                w(f"      v1[{r}] = cscale({pre}A{r}, v0[{r}]);")
+                                w(f"      v1[{r}] = cscale({coef[r]}, v0[{r}]);")
                         if slot >= 0:
                             w("      " + gs_store(slot - slb, "e"))
                     w("    }")

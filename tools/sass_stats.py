@@ -27,9 +27,19 @@ def programs(name):
         circ = wl.rcs_circuits(1, 24, 20)[0]
         from paper_2003_02989_b200.pauli import PauliSum, PauliString
         cost = PauliSum([PauliString(1.0, {q: "Z"}) for q in range(24)])
+    elif name == "qcnn":
+        from paper_2003_02989_b200.circuit import Circuit
+        from paper_2003_02989_b200.pauli import PauliSum, PauliString
+        phis, _, _ = wl.qcnn_data(4, 16)
+        model = wl.qcnn_model(16)
+        circ = Circuit(16, list(wl.qcnn_data_circuit(phis[0]).gates) + list(model.gates))
+        cost = PauliSum([PauliString(1.0, {15: "Z"})])
+    elif name == "hea":
+        circ = wl.hea_circuit(16, 4)
+        cost = wl.z_sum(16)
     else:
         raise SystemExit(f"unknown workload {name}")
-    syms = circuit_symbols(circ)
+    syms = circuit_symbols(circ) if name != "qcnn" else circuit_symbols(model)
     si = {s: i for i, s in enumerate(syms)}
     obs = analyse_observables([cost])
     infos = pl.analyse(circ, si)
