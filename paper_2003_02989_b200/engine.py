@@ -178,7 +178,11 @@ class Bound:
         sym_index = {s: i for i, s in enumerate(self.symbol_names)}
         self.circuits = list(circuits)
         template = self.circuits[0]
+        seen = set()
         for c in self.circuits:
+            if id(c) in seen:
+                continue
+            seen.add(id(c))
             if c.num_qubits != template.num_qubits:
                 raise ValueError("all circuits of a batch must have the same register size")
             for s in circuit_symbols(c):

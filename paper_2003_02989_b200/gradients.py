@@ -176,6 +176,49 @@ def _ps_expand(circuit, bindings, symbols):
     return Circuit(circuit.num_qubits, gates), names, np.array(vals, dtype=np.float64), occ
 
 
+_PS_CACHE: dict = {}
+
+
+def _ps_structure(circuit, symbols):
+    """Value-independent part of :func:`_ps_expand`: (expanded circuit, pseudo-symbol names,
+    spec [(symbol index, coeff, const, beta)] per pseudo-symbol, occ).  base[b, k] =
+    (coeff * theta[b, sym] + const) * beta for every row at once.  Cached per circuit object
+    (circuits are immutable), so repeated calls reuse one engine binding."""
+    key = (id(circuit), tuple(symbols))
+    hit = _PS_CACHE.get(key)
+    if hit is not None and hit[0] is circuit:
+        return hit[1]
+    out = _ps_structure_build(circuit, symbols)
+    if len(_PS_CACHE) > 256:
+        _PS_CACHE.clear()
+    _PS_CACHE[key] = (circuit, out)
+    return out
+
+
+def _ps_structure_build(circuit, symbols):
+    index = {s: i for i, s in enumerate(symbols)}
+    gates, names, spec, occ = [], [], [], []
+    for j, g in enumerate(circuit.gates):
+        e = g.exponent
+        if e is None or e.symbol is None:
+            gates.append(g)
+            continue
+        gen = as_pauli_sum(g.generator)
+        if not all_terms_commute(gen):
+            raise ValueError(f"gate {j}: generator terms do not commute, so the parameter-shift "
+                             "rule does not apply — use finite_difference_grad instead")
+        for t in gen.terms:
+            if not t.factors or t.coefficient == 0.0:
+                continue
+            name = f"__ps{j}_{len(names)}"
+            gates.append(Gate(tuple(sorted(t.factors)), exponent=ParamExpr(name),
+                              generator=PauliSum([PauliString(1.0, t.factors)])))
+            names.append(name)
+            spec.append((index[e.symbol], float(e.coeff), float(e.const), float(t.coefficient)))
+            occ.append((index[e.symbol], e.coeff * t.coefficient))
+    return Circuit(circuit.num_qubits, gates), names, spec, occ
+
+
 def _ps_rows(base, k_count):
     rows = np.repeat(base[None, :], 2 * k_count, axis=0)
     for k in range(k_count):

@@ -425,3 +425,25 @@ def test_large_register_30q_norm_and_sharding(cuda):
     got, _ = D.run_sharded(c, obs, 1, D.LoopbackExchange(1))
     assert got == pytest.approx(want, abs=1e-5)
     torch.cuda.empty_cache()
+
+
+def test_batched_parameter_shift_matches_reference_ps(cuda, golden):
+    """ops.expectation_and_ps_gradient (all rows x shifts batched) against the reference's
+    parameter-shift vectors (golden HEA config rows) and the oracle's PS on random rows."""
+    meta, arr = golden
+    cfg = meta["configs"]["hea"]
+    c = from_json(cfg["circuit"])
+    o = _obs(cfg["observable"])
+    rows = np.array(cfg["rows"], dtype=np.float32)
+    e, g = ops.expectation_and_ps_gradient(c, circuit_symbols(c), rows, [o])
+    np.testing.assert_allclose(e, arr["hea/exp"], atol=EXP)
+    _close_grad(g, arr["hea/ps"])
+    rng = np.random.default_rng(44)
+    c2 = random_circuit(rng, 6, 60, n_sym=4)
+    syms = circuit_symbols(c2)
+    th = rng.uniform(-2, 2, size=(3, len(syms))).astype(np.float32)
+    o2 = random_observable(rng, 6)
+    e2, g2 = ops.expectation_and_ps_gradient([c2] * 3, syms, th, [o2])
+    for b in range(3):
+        bind = dict(zip(syms, th[b].astype(np.float64)))
+        _close_grad(g2[b], orc.parameter_shift_grad(c2, o2, bind)[0])
