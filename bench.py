@@ -282,8 +282,9 @@ def run_gpu(args, rank, world):
     struct_a.coef_row_stride = hw.shape[1]
     fb, ab = pass_bytes(fw.prog, B), pass_bytes(ad.prog, B)
     jf, ja = fw.jit(dev, B), ad.jit(dev, B)
-    kname = ("plan-specialised NVRTC tile-pass kernels qf_f_p*/qf_a_p* (forward L13/R5, adjoint L12/R4)"
-             if jf is not None else "qf::pass_kernel (forward L13/R5 + adjoint L12/R4)")
+    kname = (f"plan-specialised NVRTC tile-pass kernels qf_f_p*/qf_a_p* (forward L{fw.prog.L}/R{fw.prog.R}, "
+             f"adjoint L{ad.prog.L}/R{ad.prog.R}, Pauli-frame normalised={bool(fw.frame)})"
+             if jf is not None else "qf::pass_kernel (interpreted)")
     reps = 3
     times_f = np.zeros(len(fb))
     times_a = np.zeros(len(ab))
