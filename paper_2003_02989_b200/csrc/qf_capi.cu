@@ -393,7 +393,8 @@ __global__ void draw_kernel(const float2* __restrict__ psi, int n, int rows, int
 //                  second form multiplies the frame by Q.  Gradient slot scale = m * sign,
 //                  sign = (-1)^{z_q} (X) or (-1)^{x_q + z_q} (Y) = P^dag Q P / Q.
 //   EV_ABS1/ABS2   general dense op: matrix absorbs the frame (M P, or P M in the adjoint
-//                  whose kernels apply M^dag), frame bits on its qubits are cleared.
+//                  whose kernels apply M^dag), frame bits on its qubits are cleared; its
+//                  gradient slot (taken after the apply, frame-free there) scales by m.
 //   EV_DIAG/OBS    frame x-mask written to the op's angle column (kernels evaluate the
 //                  phase polynomial / observable at index ^ x); slot scale = m.
 // ---------------------------------------------------------------------------
@@ -484,6 +485,7 @@ __global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int 
           N[i * D + j] = acc;
         }
       for (int i = 0; i < D * D; ++i) M[off + i] = make_float2((float)N[i].x, (float)N[i].y);
+      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = m;  // gradient taken after the apply
     } else if (kind == 5 || kind == 6) {
       angles[(size_t)row * n_ang + col] = (int32_t)x;
       if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = m;

@@ -424,7 +424,7 @@ class Engine:
         overrides = overrides or {}
         topo = pl.topology_key(template, symbol_index)
         key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state, frame,
-               tuple(sorted(overrides.items())))
+               tuple(sorted(overrides.items())), pl.FUSION_ENABLED)
         with self._lock:
             hit = self._plans.get(key)
         if hit is not None:
@@ -459,7 +459,7 @@ class Engine:
         symbol_names = tuple(s.name if hasattr(s, "name") else s for s in symbol_names)
         observables = list(observables)
         key = (tuple(map(id, circuits)), symbol_names, tuple(map(id, observables)), bool(want_grad), str(dev),
-               bool(from_state), bool(want_state), bool(norm_identity))
+               bool(from_state), bool(want_state), bool(norm_identity), pl.FUSION_ENABLED)
         with self._lock:
             hit = self._bound.get(key)
         if hit is not None and all(a is b for a, b in zip(hit.circuits, circuits)):

@@ -268,36 +268,40 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                         w(f"      applyN<{s0}, {NR}, {ax}>(v1, tau);")
                     w(f"      applyN<{s0}, {NR}, {ax}>(v0, tau); }}")
                 elif kind == pl.OP_DENSE1:
+                    # adjoint: apply U^dag first, then the gradient slot -- G commutes with
+                    # U = exp(-i v G), so Im<lam|G|psi> is the same on either side, and after
+                    # the apply the Pauli frame on the op's qubits has been absorbed
                     w(f"    {{ const float2 u00 = M[{moff}], u01 = M[{moff + 1}], u10 = M[{moff + 2}], u11 = M[{moff + 3}];")
-                    if adj:
-                        if slot >= 0:
-                            g0 = int(op[8])
-                            if gk:
-                                sc = float(gm[g0 + 4, 0])
-                                w(f"      const float gacc = {_flit(sc)} * gradp<{s0}, {NR}, {gk}>(v0, v1);")
-                            else:
-                                gl = [f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})" for i in range(4)]
-                                w(f"      const float gacc = grad1<{s0}, {NR}>(v0, v1, {', '.join(gl)});")
-                            w("      " + gs_store(slot - slb, "gacc"))
-                        if cls == pl.CLS_GENERAL:
-                            w(f"      apply1m<{s0}, {NR}>(v1, M + {moff}, MN + {moff});")
-                        else:
-                            w(f"      apply1<{s0}, {NR}, {cls}>(v1, u00, u01, u10, u11);")
                     if cls == pl.CLS_GENERAL:
-                        w(f"      apply1m<{s0}, {NR}>(v0, M + {moff}, MN + {moff}); }}")
+                        if adj:
+                            w(f"      apply1m<{s0}, {NR}>(v1, M + {moff}, MN + {moff});")
+                        w(f"      apply1m<{s0}, {NR}>(v0, M + {moff}, MN + {moff});")
                     else:
-                        w(f"      apply1<{s0}, {NR}, {cls}>(v0, u00, u01, u10, u11); }}")
+                        if adj:
+                            w(f"      apply1<{s0}, {NR}, {cls}>(v1, u00, u01, u10, u11);")
+                        w(f"      apply1<{s0}, {NR}, {cls}>(v0, u00, u01, u10, u11);")
+                    if adj and slot >= 0:
+                        g0 = int(op[8])
+                        if gk:
+                            sc = float(gm[g0 + 4, 0])
+                            w(f"      const float gacc = {_flit(sc)} * gradp<{s0}, {NR}, {gk}>(v0, v1);")
+                        else:
+                            gl = [f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})" for i in range(4)]
+                            w(f"      const float gacc = grad1<{s0}, {NR}>(v0, v1, {', '.join(gl)});")
+                        w("      " + gs_store(slot - slb, "gacc"))
+                    w("    }")
                 elif kind == pl.OP_DENSE2:
                     if adj:
                         w("    {")
+                        w(f"      apply2m<{s0}, {s1}, {NR}>(v0, M + {moff}, MN + {moff});"
+                          f" apply2m<{s0}, {s1}, {NR}>(v1, M + {moff}, MN + {moff});")
                         if slot >= 0:
                             g0 = int(op[8])
                             gl = ", ".join(f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})"
                                            for i in range(16))
                             w(f"      const float2 g[16] = {{{gl}}};")
                             w("      " + gs_store(slot - slb, f"grad2<{s0}, {s1}, {NR}>(v0, v1, g)"))
-                        w(f"      apply2m<{s0}, {s1}, {NR}>(v0, M + {moff}, MN + {moff});"
-                          f" apply2m<{s0}, {s1}, {NR}>(v1, M + {moff}, MN + {moff}); }}")
+                        w("    }")
                     else:
                         w(f"    apply2m<{s0}, {s1}, {NR}>(v0, M + {moff}, MN + {moff});")
                 elif kind in (pl.OP_DIAG, pl.OP_OBS):

@@ -262,12 +262,26 @@ def _diag_op_qubits(gates, infos):
     return tuple(sorted(qs))
 
 
+FUSION_ENABLED = True   # False: one op per gate (the reference's fuse_enabled=False cells)
+
+
 def build_ops(infos: list[GateInfo], adjoint: bool) -> list[Op]:
     """Fuse gates into dense 1q/2q ops and diagonal phase-polynomial ops.
 
     ``adjoint``: symbolic gates are never merged with anything except that
     symbolic diagonal gates sharing one symbol share a DIAG op.
     """
+    if not FUSION_ENABLED:
+        out = []
+        for gi, info in enumerate(infos):
+            if info.diag:
+                out.append(Op(OP_DIAG, tuple(sorted(info.targets)), gates=[gi], symbolic=info.symbolic,
+                              sym=info.sym if info.symbolic else -1))
+            else:
+                out.append(Op(OP_DENSE1 if len(info.targets) == 1 else OP_DENSE2, tuple(info.targets),
+                              factors=[gi], symbolic=info.symbolic, sym=info.sym if info.symbolic else -1))
+            out[-1].index = len(out) - 1
+        return out
     ops: list[Op | None] = []
     last: dict[int, int] = {}   # qubit -> index of last op touching it
 
@@ -711,14 +725,10 @@ def _walsh_angles(diag_entries: np.ndarray) -> np.ndarray:
 
 
 def frame_eligible(ops: list[Op], infos, adjoint: bool) -> bool:
-    """Pauli-frame normalisation needs every gradient-carrying dense op to be a single-qubit
-    X/Y rotation (its generator then only changes sign under the frame)."""
-    if not adjoint:
-        return True
-    for op in ops:
-        if op.kind in (OP_DENSE1, OP_DENSE2) and op.symbolic:
-            if op.kind != OP_DENSE1 or any(infos[gi].axis not in ("X", "Y") for gi in op.factors):
-                return False
+    """Every program qualifies: normalised X/Y rotations carry their generator's frame sign
+    in the slot scale; any other gradient-carrying dense op absorbs the frame into its matrix
+    and evaluates its gradient after applying U^dag (G commutes with U), where the frame on
+    its qubits is the identity."""
     return True
 
 
@@ -838,6 +848,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         axes = {infos[gi].axis for gi in op.factors}
                         if frame and len(axes) == 1 and axes <= {"X", "Y"}:
                             orow[9] = CLS_NX if axes == {"X"} else CLS_NY
+                        elif frame and orow[9] == CLS_XLIKE:
+                            orow[9] = CLS_GENERAL   # an absorbed X frame breaks the X-like structure
+                                                    # (real matrices stay real under X^a Z^b)
                     ev = None
                     if frame:
                         if op.kind == OP_DENSE1:

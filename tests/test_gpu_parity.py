@@ -340,8 +340,9 @@ def test_plan_specialised_kernels_match_interpreter(cuda, monkeypatch):
     _close_grad(out["1"][2][0], gg)
 
 
-@pytest.mark.parametrize("seed,n", [(0, 11), (1, 13), (2, 14)])
-def test_pauli_frame_normalised_programs_vs_oracle(cuda, monkeypatch, seed, n):
+@pytest.mark.parametrize("seed,n,family", [(0, 11, "rot"), (1, 13, "rot"), (2, 14, "rot"), (3, 12, "any"),
+                                           (4, 13, "any")])
+def test_pauli_frame_normalised_programs_vs_oracle(cuda, monkeypatch, seed, n, family):
     """Plan-specialised kernels with Pauli-frame normalised rotations (engine default for
     diagonal observables): expectations and adjoint gradients against the oracle, and
     identical to the same kernels without the frame (QF_FRAME=0)."""
@@ -349,7 +350,7 @@ def test_pauli_frame_normalised_programs_vs_oracle(cuda, monkeypatch, seed, n):
     from paper_2003_02989_b200.engine import ENGINE
 
     rng = np.random.default_rng(300 + seed)
-    c = rotation_circuit(rng, n, 220, n_sym=6)
+    c = rotation_circuit(rng, n, 220, n_sym=6) if family == "rot" else random_circuit(rng, n, 200, n_sym=5)
     syms = circuit_symbols(c)
     theta = rng.uniform(-3.5, 3.5, size=(4, len(syms))).astype(np.float32)
     obs = [random_observable(rng, n, diag=True, k=6), random_observable(rng, n, diag=True, k=3)]
