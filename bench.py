@@ -351,7 +351,9 @@ def run_gpu(args, rank, world):
         cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"]}
 
     if rank == 0:
-        launches = len(fb) + len(ab) + 2 + 3  # passes + 2 builds + 3 slot reductions
+        # passes + 2 x (dense + angle build) + frame walks + 3 slot reductions (expectation,
+        # gradient, energy); cross-checked against the ncu launch list (profiles/)
+        launches = len(fb) + len(ab) + 4 + (2 if fw.frame else 0) + 3
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

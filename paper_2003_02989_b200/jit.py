@@ -56,6 +56,42 @@ def _xor_expr(bits: list, var: str = "t") -> str:
     return "(" + " ^ ".join(parts) + ")" if parts else "0u"
 
 
+def _int_poly(prog, tb: int, te: int):
+    """A DIAG op whose angles are all integer multiples m_k of one runtime angle (one symbol,
+    one affine map, beta_k = m_k beta_0 -- e.g. a QAOA cost layer): returns (base angle
+    column, [m_k], H = sum |m_k|) so the phase exp(-i a0 h) with h = sum_k m_k chi_k is a
+    lookup in a per-CTA table of 2H+1 entries; else None."""
+    r = prog.recipe
+    tsrc = np.asarray(r["term_src"]).reshape(-1, 2)
+    tbeta = np.asarray(r["term_beta"])
+    cols = [int(prog.term_idx[kk]) for kk in range(tb, te)]
+    if not cols:
+        return None
+    key = None
+    for col in cols:
+        kind, src = int(tsrc[col][0]), int(tsrc[col][1])
+        if kind != 0:
+            return None
+        k = (int(r["gen_sym"][src]), float(r["gen_coeff"][src]), float(r["gen_const"][src]))
+        if key is None:
+            key = k
+        elif k != key:
+            return None
+    base = min(cols, key=lambda c: abs(float(tbeta[c])))
+    b0 = float(tbeta[base])
+    if b0 == 0.0:
+        return None
+    ms = []
+    for col in cols:
+        ratio = float(tbeta[col]) / b0
+        m = int(round(ratio))
+        if m == 0 or abs(ratio - m) > 1e-9:
+            return None
+        ms.append(m)
+    H = sum(abs(m) for m in ms)
+    return (base, ms, H) if H <= 255 else None
+
+
 def _wht_code(vals: dict, R: int, kind: str, out: str, indent: str) -> list:
     """Walsh-Hadamard transform over 2^R entries with symbolic zero tracking.
     vals: S -> variable name (entries absent are zero).  Emits `out{r}` variables."""
@@ -75,14 +111,14 @@ def _wht_code(vals: dict, R: int, kind: str, out: str, indent: str) -> list:
             if y is None:
                 lines.append(f"{indent}const {kind} {a} = {x}, {b} = {x};")
             elif x is None:
-                neg = f"(0u - {y})" if kind == "u32" else f"(-{y})"
+                neg = f"(0u - {y})" if kind == "u32" else f"(-{y})"  # int / float: plain negation
                 lines.append(f"{indent}const {kind} {a} = {y}, {b} = {neg};")
             else:
                 lines.append(f"{indent}const {kind} {a} = {x} + {y}, {b} = {x} - {y};")
             nxt[r] = a
             nxt[r | (1 << j)] = b
         cur = nxt
-    zero = "0u" if kind == "u32" else "0.f"
+    zero = {"u32": "0u", "int": "0"}.get(kind, "0.f")
     for r in range(1 << R):
         lines.append(f"{indent}const {kind} {out}{r} = {cur.get(r, zero)};")
     return lines
@@ -118,6 +154,26 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         per_thread_gs = scnt * NT * 4 <= GS_THREAD_BYTES
         GSW = NT if per_thread_gs else NT // 32
         smem = NA * TILE * 8 + mcnt * 16 + acnt * 4 + ccnt * 4 + scnt * GSW * 4 + 16
+        # integer-weight phase polynomials (full-WHT path only) get a per-CTA phase table
+        int_tables = {}
+        tbl_bytes = 0
+        for s_ in range(sb, se):
+            stg = prog.stages[s_]
+            rg = [int(stg[j]) for j in range(R)]
+            for k_ in range(int(stg[48]), int(stg[49])):
+                op_ = prog.ops[k_]
+                if int(op_[0]) != pl.OP_DIAG:
+                    continue
+                subs = {pl._bit_subset(int(prog.term_mask[kk]), rg) for kk in range(int(op_[4]), int(op_[5]))}
+                kb = {j for S_ in subs for j in range(R) if S_ >> j & 1}
+                if (1 << len(kb)) < NR:
+                    continue
+                ip = _int_poly(prog, int(op_[4]), int(op_[5]))
+                if ip is None or ip[0] < ab or ip[0] >= ae:
+                    continue
+                int_tables[k_] = (ip, tbl_bytes)
+                tbl_bytes += (2 * ip[2] + 1) * 16
+        smem = (smem + 15) // 16 * 16 + tbl_bytes
         pass_ops = [prog.ops[k] for s_ in range(sb, se) for k in range(int(prog.stages[s_][48]),
                                                                         int(prog.stages[s_][49]))]
         heavy = any(int(op_[0]) == pl.OP_DENSE2 or (int(op_[0]) == pl.OP_DENSE1 and int(op_[9]) == pl.CLS_GENERAL)
@@ -139,6 +195,8 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         w(f"  int* ANG = reinterpret_cast<int*>(MN + {mcnt});")
         w(f"  float* CO = reinterpret_cast<float*>(ANG + {acnt});")
         w(f"  float* GS = CO + {ccnt};")
+        if int_tables:
+            w(f"  float4* TB = reinterpret_cast<float4*>(smem_raw + {(smem - tbl_bytes)});")
         w("  const u32 t = threadIdx.x;")
         w(f"  const int row = (int)(blockIdx.x >> {n - L});")
         w(f"  const u32 o = blockIdx.x & {(1 << (n - L)) - 1}u;")
@@ -171,6 +229,12 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         if adj:
             w(f"  float2 v1[{NR}];")
         w("  __syncthreads();")
+        if int_tables:
+            for k_, ((bcol, ms, H), off) in int_tables.items():
+                w(f"  for (int h = t; h < {2 * H + 1}; h += {NT}) {{ const float2 ph = phase_turns("
+                  f"(int)((u32)(h - {H}) * (u32)ANG[{bcol - ab}]), {'true' if adj else 'false'});"
+                  f" TB[{off // 16} + h] = make_float4(ph.x, ph.x, -ph.y, ph.y); }}")
+            w("  __syncthreads();")
 
         st_rows = [prog.stages[s] for s in range(sb, se)]
 
@@ -338,7 +402,29 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                         e = " ".join(parts)
                         return e[1:] if e[0] == "+" else "(" + zero + " " + e + ")"
 
-                    if kind == pl.OP_DIAG:
+                    if kind == pl.OP_DIAG and k in int_tables:
+                        (bcol, ms, H), off = int_tables[k]
+                        kks = list(range(tb, te))
+                        for S, ks in groups.items():
+                            w(f"      int {pre}h{S} = 0;")
+                            for kk in ks:
+                                m = int(prog.term_mask[kk])
+                                mk = ms[kks.index(kk)]
+                                w(f"      {pre}h{S} += (__popc({gv} & {m}u) & 1) ? {-mk} : {mk};")
+                        o.extend(_wht_code({S: f"{pre}h{S}" for S in groups}, R, "int", f"{pre}H", "      "))
+                        if adj and slot >= 0:
+                            wb = float(prog.term_w[tb + ms.index(min(ms, key=abs))]) / min(ms, key=abs)
+                            w("      float gq = 0.f;")
+                            for r in range(NR):
+                                w(f"      gq = fmaf((float){pre}H{r}, im_conj_mul(v1[{r}], v0[{r}]), gq);")
+                            w("      " + gs_store(slot - slb, f"{_flit(wb)} * gq"))
+                        for r in range(NR):
+                            w(f"      {{ const float4 T = TB[{off // 16 + H} + {pre}H{r}];"
+                              f" const u64 P = pk(T.x, T.y), N = pk(T.z, T.w);"
+                              f" v0[{r}] = upk(f2fma(N, pk(v0[{r}].y, v0[{r}].x), f2mul(P, pk(v0[{r}].x, v0[{r}].y))));" +
+                              (f" v1[{r}] = upk(f2fma(N, pk(v1[{r}].y, v1[{r}].x), f2mul(P, pk(v1[{r}].x, v1[{r}].y))));"
+                               if adj else "") + " }")
+                    elif kind == pl.OP_DIAG:
                         if adj and slot >= 0:
                             bnames = {}
                             for S, ks in groups.items():
