@@ -454,6 +454,48 @@ __global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int 
         if (kind == 2) z ^= bit;
       }
       M[off] = make_float2((float)tau, 0.f);
+    } else if (kind == 7) {  // normalised two-qubit Pauli-string rotation on (q0 msb, q1 lsb)
+      const int code = E[6];
+      const int l0 = code & 3, l1 = (code >> 2) & 3;  // 1 X, 2 Y, 3 Z
+      const uint32_t b0 = 1u << q0, b1 = 1u << q1;
+      // F^dag P F = sign P: X/Y anticommute with a Z frame bit, Y/Z with an X frame bit
+      int flip = 0;
+      flip ^= ((l0 == 1 || l0 == 2) && (z & b0)) ? 1 : 0;
+      flip ^= ((l0 == 2 || l0 == 3) && (x & b0)) ? 1 : 0;
+      flip ^= ((l1 == 1 || l1 == 2) && (z & b1)) ? 1 : 0;
+      flip ^= ((l1 == 2 || l1 == 3) && (x & b1)) ? 1 : 0;
+      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = flip ? -m : m;
+      // U = e^{i phi}(c I - i s P):  U[0][0] = e^{i phi} c,  U[xm][0] = -i s c0 e^{i phi} with
+      // P|00> = c0 |xm>  (c0 = i per Y factor);  the adjoint uses U^dag: (U^dag)[xm][0] = conj(U[0][xm])
+      const int xm = ((l0 == 1 || l0 == 2) ? 2 : 0) | ((l1 == 1 || l1 == 2) ? 1 : 0);
+      const int ny = (l0 == 2) + (l1 == 2);
+      Z u00 = {M[off].x, M[off].y}, uxm;
+      if (adjoint) {
+        u00.y = -u00.y;
+        uxm = {M[off + xm].x, -M[off + xm].y};
+      } else {
+        uxm = {M[off + xm * 4].x, M[off + xm * 4].y};
+      }
+      // s e^{i phi} = U[xm][0] * i / c0 = U[xm][0] * i * conj(i^ny)
+      Z sv = {-uxm.y, uxm.x};                      // * i
+      for (int k = 0; k < ny; ++k) sv = {sv.y, -sv.x};  // * (-i) per Y
+      const double c2 = u00.x * u00.x + u00.y * u00.y, s2 = sv.x * sv.x + sv.y * sv.y;
+      double tau;
+      if (c2 >= s2) {
+        tau = (sv.x * u00.x + sv.y * u00.y) / c2;
+        if (flip) tau = -tau;
+        m *= c2;
+      } else {
+        double k = (u00.x * sv.x + u00.y * sv.y) / s2;
+        if (flip) k = -k;
+        tau = -k;
+        m *= s2;
+        if (l0 == 1 || l0 == 2) x ^= b0;
+        if (l0 == 2 || l0 == 3) z ^= b0;
+        if (l1 == 1 || l1 == 2) x ^= b1;
+        if (l1 == 2 || l1 == 3) z ^= b1;
+      }
+      M[off] = make_float2((float)tau, 0.f);
     } else if (kind == 3 || kind == 4) {  // absorb the frame into a general dense op
       const int D = kind == 3 ? 2 : 4;
       Z P[16];

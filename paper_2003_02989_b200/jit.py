@@ -354,6 +354,16 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                             w(f"      const float gacc = grad1<{s0}, {NR}>(v0, v1, {', '.join(gl)});")
                         w("      " + gs_store(slot - slb, "gacc"))
                     w("    }")
+                elif kind == pl.OP_DENSE2 and cls == pl.CLS_NP:
+                    code = int(op[12])
+                    w(f"    {{ const float tau = M[{moff}].x;")
+                    if adj and slot >= 0:
+                        g0 = int(op[8])
+                        sc = float(gm[g0 + 16, 0])
+                        w("      " + gs_store(slot - slb, f"{_flit(sc)} * gradNP<{s0}, {s1}, {NR}, {code}>(v0, v1)"))
+                    if adj:
+                        w(f"      applyNP<{s0}, {s1}, {NR}, {code}>(v1, tau);")
+                    w(f"      applyNP<{s0}, {s1}, {NR}, {code}>(v0, tau); }}")
                 elif kind == pl.OP_DENSE2:
                     if adj:
                         w("    {")

@@ -51,9 +51,12 @@ def geometry(adjoint: bool) -> tuple:
 OP_DENSE1, OP_DENSE2, OP_DIAG, OP_OBS = 1, 2, 3, 4
 CLS_GENERAL, CLS_XLIKE, CLS_REAL = 0, 1, 2   # dense 1q matrix structure classes
 CLS_NX, CLS_NY = 3, 4                       # Pauli-frame normalised X / Y rotations: [[1, -i tau], [-i tau, 1]] / [[1, -tau], [tau, 1]]
-EV_NX, EV_NY, EV_ABS1, EV_ABS2, EV_DIAG, EV_OBS = 1, 2, 3, 4, 5, 6   # frame-walk events
+CLS_NP = 5                                  # normalised two-qubit Pauli-string rotation I - i tau P0 P1
+EV_NX, EV_NY, EV_ABS1, EV_ABS2, EV_DIAG, EV_OBS, EV_NP = 1, 2, 3, 4, 5, 6, 7   # frame-walk events
+PAULI_CODE = {"X": 1, "Y": 2, "Z": 3}
 EV_INTS = 8
-GK_MATRIX, GK_X, GK_Y, GK_Z = 0, 1, 2, 3     # adjoint generator kinds
+GK_MATRIX, GK_X, GK_Y, GK_Z = 0, 1, 2, 3     # adjoint generator kinds (GK_P: two-qubit Pauli string)
+GK_P = 4
 INIT_LOAD, INIT_ZERO, INIT_PRODUCT, INIT_LOAD_PSI = 0, 1, 2, 3
 
 STAGE_INTS, OP_INTS, PASS_INTS = 64, 16, 128
@@ -84,6 +87,7 @@ class GateInfo:
     const_col: int = -1    # first constant-angle column (concrete diagonal gates)
     cls: int = CLS_GENERAL  # dense 1q structure class (same for every row of a topology)
     axis: str = ""          # "X" / "Y": a 1q rotation exp(-i v P) (+ global phase) -> frame-normalisable
+    pstring: tuple = ()     # 2q rotation exp(-i v beta P0 P1) (+ identity): ((q0, letter), (q1, letter))
 
 
 def _is_z_only(terms) -> bool:
@@ -113,6 +117,20 @@ def _rotation_axis(terms, targets) -> str:
         return ""
     a = letters.pop()
     return a if a in ("X", "Y") else ""
+
+
+def _pauli_string(terms, targets) -> tuple:
+    """((q0, P0), (q1, P1)) when the generator is one two-qubit, non-diagonal Pauli string
+    (plus an identity term)."""
+    if len(targets) != 2:
+        return ()
+    plain = [(f, c) for f, c in terms if f and c != 0.0]
+    if len(plain) != 1 or set(plain[0][0]) != set(targets):
+        return ()
+    f = plain[0][0]
+    if all(p == "Z" for p in f.values()):
+        return ()
+    return tuple((q, f[q]) for q in targets)
 
 
 def _matrix_class(m) -> int:
@@ -226,7 +244,7 @@ def analyse(circuit, symbol_index, overrides=None) -> list[GateInfo]:
             terms = _gate_terms(g)
             infos.append(GateInfo(i, tg, True, _is_z_only(terms), symbol_index[e.symbol],
                                   float(e.coeff), float(e.const), terms, cls=_symbolic_class(terms, tg),
-                                  axis=_rotation_axis(terms, tg)))
+                                  axis=_rotation_axis(terms, tg), pstring=_pauli_string(terms, tg)))
         else:
             d = _concrete_is_diag(g)
             ax = "" if (d or g.matrix is not None) else _rotation_axis(_gate_terms(g), tg)
@@ -851,11 +869,21 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         elif frame and orow[9] == CLS_XLIKE:
                             orow[9] = CLS_GENERAL   # an absorbed X frame breaks the X-like structure
                                                     # (real matrices stay real under X^a Z^b)
+                    else:
+                        orow[9] = CLS_GENERAL
+                        if frame and len(op.factors) == 1 and infos[op.factors[0]].symbolic and \
+                                infos[op.factors[0]].pstring:
+                            orow[9] = CLS_NP
                     ev = None
                     if frame:
                         if op.kind == OP_DENSE1:
                             kind = {CLS_NX: EV_NX, CLS_NY: EV_NY}.get(int(orow[9]), EV_ABS1)
                             ev = [kind, order[0], -1, int(orow[3]), -1, -1, 0, 0]
+                        elif orow[9] == CLS_NP:
+                            ps = dict(infos[op.factors[0]].pstring)
+                            code = PAULI_CODE[ps[order[0]]] | (PAULI_CODE[ps[order[1]]] << 2)
+                            orow[12] = code
+                            ev = [EV_NP, order[0], order[1], int(orow[3]), -1, -1, code, 0]
                         else:
                             ev = [EV_ABS2, order[0], order[1], int(orow[3]), -1, -1, 0, 0]
                     if adjoint and op.symbolic:
@@ -865,7 +893,8 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         gm = gm * (2.0 * info.coeff)
                         orow[8] = len(em.genmats) // 2
                         em.genmats.extend(np.stack([gm.real, gm.imag], -1).reshape(-1).tolist())
-                        orow[10] = _generator_kind(info.terms) if op.kind == OP_DENSE1 else GK_MATRIX
+                        orow[10] = _generator_kind(info.terms) if op.kind == OP_DENSE1 else \
+                            (GK_P if orow[9] == CLS_NP else GK_MATRIX)
                         if orow[10] != GK_MATRIX:   # single Pauli: its scaled coefficient follows the matrix
                             beta = sum(c for f, c in info.terms if f)
                             em.genmats.extend([2.0 * info.coeff * beta, 0.0])
