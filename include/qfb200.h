@@ -212,6 +212,8 @@ void qf_jit_free(void* p);
 int qf_jit_load(const void* image, void** module);
 int qf_jit_function(void* module, const char* name, int max_dyn_smem, void** func);
 int qf_jit_unload(void* module);
+/* Resident CTAs per SM of a loaded pass kernel (grid size of the persistent kernels). */
+int qf_jit_occupancy(void* func, int block, int dyn_smem, int* blocks_per_sm);
 /* Launch n generated pass kernels in order on `stream` with one packed argument struct
  * (QfJitArgs in csrc/qf_jit_prelude.cuh). */
 int qf_jit_run(void* const* funcs, const uint32_t* grid, const uint32_t* block, const uint32_t* smem, int n,

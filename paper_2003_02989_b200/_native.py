@@ -17,7 +17,7 @@ EXPORTS = (
     "qf_last_error", "qf_version", "qf_device_sm_count", "qf_build_ops", "qf_run_passes",
     "qf_adjoint_passes", "qf_reduce_slots", "qf_pauli_expect", "qf_pauli_apply", "qf_sample",
     "qf_jit_compile", "qf_jit_free", "qf_jit_load", "qf_jit_function", "qf_jit_unload", "qf_jit_run",
-    "qf_reduce_slots_scaled", "qf_frame_walk",
+    "qf_reduce_slots_scaled", "qf_frame_walk", "qf_jit_occupancy",
 )
 
 _p = C.c_void_p
@@ -87,6 +87,7 @@ def load(build_if_missing: bool = True):
     lib.qf_jit_load.argtypes = [_p, C.POINTER(C.c_void_p)]
     lib.qf_jit_function.argtypes = [_p, C.c_char_p, C.c_int, C.POINTER(C.c_void_p)]
     lib.qf_jit_unload.argtypes = [_p]
+    lib.qf_jit_occupancy.argtypes = [_p, C.c_int, C.c_int, C.POINTER(C.c_int)]
     lib.qf_jit_run.argtypes = [_p, _p, _p, _p, C.c_int, _p, _p, C.c_size_t]
     for name in EXPORTS:
         getattr(lib, name).restype = C.c_int if name != "qf_last_error" else C.c_char_p

@@ -44,6 +44,7 @@ class QfJitArgs(C.Structure):
 
 
 GS_THREAD_BYTES = 40 * 1024
+PERSIST = os.environ.get("QF_PERSIST", "0") not in ("0", "", "false", "no")   # measured slower (no prefetch)
 
 
 def _flit(x: float) -> str:
@@ -198,8 +199,26 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         if int_tables:
             w(f"  float4* TB = reinterpret_cast<float4*>(smem_raw + {(smem - tbl_bytes)});")
         w("  const u32 t = threadIdx.x;")
-        w(f"  const int row = (int)(blockIdx.x >> {n - L});")
-        w(f"  const u32 o = blockIdx.x & {(1 << (n - L)) - 1}u;")
+        if PERSIST:
+            # persistent CTAs: a contiguous run of tiles each, so the row's staged matrices,
+            # angles and phase tables are rebuilt only when the row changes
+            w(f"  const u32 total = (u32)a.pad << {n - L};")
+            w("  const u32 per = (total + gridDim.x - 1) / gridDim.x;")
+            w("  u32 tile = blockIdx.x * per;")
+            w("  const u32 tend = min(total, tile + per);")
+            w("  int cur = -1;")
+            w(f"  float2 v0[{NR}];")
+            if adj:
+                w(f"  float2 v1[{NR}];")
+            w("  for (; tile < tend; ++tile) {")
+            w(f"  const int row = (int)(tile >> {n - L});")
+            w(f"  const u32 o = tile & {(1 << (n - L)) - 1}u;")
+            w("  if (row != cur) {")
+            w("  cur = row;")
+            w("  __syncthreads();")
+        else:
+            w(f"  const int row = (int)(blockIdx.x >> {n - L});")
+            w(f"  const u32 o = blockIdx.x & {(1 << (n - L)) - 1}u;")
         if mcnt:
             # stage the row's matrices: as built for the forward sweep; conjugate-transposed
             # (U^dag) for general / X-like / real dense ops of the adjoint sweep
@@ -220,14 +239,10 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
             w(f"  for (int i = t; i < {acnt}; i += {NT}) ANG[i] = a.angles[(size_t)row * a.n_ang + {ab} + i];")
         if ccnt:
             w(f"  for (int i = t; i < {ccnt}; i += {NT}) CO[i] = a.coefs[(size_t)row * a.coef_stride + {cb} + i];")
-        base = " | ".join(f"(((o >> {i}) & 1u) << {q})" for i, q in enumerate(outer)) or "0u"
-        w(f"  const u32 base = {base};")
-        w(f"  float2* __restrict__ psi = a.psi + ((size_t)row << {n});")
-        if adj:
-            w(f"  float2* __restrict__ lam = a.lam + ((size_t)row << {n});")
-        w(f"  float2 v0[{NR}];")
-        if adj:
-            w(f"  float2 v1[{NR}];")
+        if not PERSIST:
+            w(f"  float2 v0[{NR}];")
+            if adj:
+                w(f"  float2 v1[{NR}];")
         w("  __syncthreads();")
         if int_tables:
             for k_, ((bcol, ms, H), off) in int_tables.items():
@@ -235,6 +250,13 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                   f"(int)((u32)(h - {H}) * (u32)ANG[{bcol - ab}]), {'true' if adj else 'false'});"
                   f" TB[{off // 16} + h] = make_float4(ph.x, ph.x, -ph.y, ph.y); }}")
             w("  __syncthreads();")
+        if PERSIST:
+            w("  }")
+        base = " | ".join(f"(((o >> {i}) & 1u) << {q})" for i, q in enumerate(outer)) or "0u"
+        w(f"  const u32 base = {base};")
+        w(f"  float2* __restrict__ psi = a.psi + ((size_t)row << {n});")
+        if adj:
+            w(f"  float2* __restrict__ lam = a.lam + ((size_t)row << {n});")
 
         st_rows = [prog.stages[s] for s in range(sb, se)]
 
@@ -531,6 +553,10 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
             w("    acc = warp_sum_d(acc);")
             w(f"    if ((t & 31) == 0) a.partials[((size_t)row * a.n_slots + {slb} + s) * {1 << (n - L)} + o] = acc;")
             w("  }")
+        if PERSIST:
+            if scnt:
+                w("  __syncthreads();   // slot partials are rewritten by the next tile")
+            w("  }")
         w("}")
         src.append("\n".join(o) + "\n")
     return src, names, geo
@@ -596,15 +622,23 @@ class JitProgram:
         self.smem = (C.c_uint32 * P)(*[g[1] for g in geo])
         self.grid = (C.c_uint32 * P)()
         self.prog = prog
+        self.persist = PERSIST
+        sms = lib.qf_device_sm_count(device_index)
+        self.resident = []
+        for f, (nt, smem) in zip(funcs, geo):
+            occ = C.c_int(0)
+            nat.check(lib.qf_jit_occupancy(f, nt, smem, C.byref(occ)))
+            self.resident.append(max(1, occ.value) * max(1, sms))
 
     def run(self, rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first=0, last=None):
         lib = nat.load()
         last = self.n if last is None else last
         args = QfJitArgs(psi=psi, lam=lam, mats=mats, angles=angles, coefs=coefs, partials=partials,
                          n_mat=self.prog.n_mat, n_ang=self.prog.n_ang, coef_stride=coef_stride,
-                         n_slots=self.prog.n_slots, tiles_log2=self.rows_shift, pad=0)
+                         n_slots=self.prog.n_slots, tiles_log2=self.rows_shift, pad=rows)
+        total = rows << self.rows_shift
         for i in range(self.n):
-            self.grid[i] = rows << self.rows_shift
+            self.grid[i] = min(total, self.resident[i]) if self.persist else total
         cnt = last - first
         nat.check(lib.qf_jit_run(C.addressof(self.funcs) + C.sizeof(C.c_void_p) * first,
                                  C.addressof(self.grid) + 4 * first, C.addressof(self.block) + 4 * first,
