@@ -409,11 +409,9 @@ __device__ void frame_pauli(int a, int b, Z (&P)[4]) {  // X^a Z^b, row-major 2x
   }
 }
 
-__global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int adjoint, int rows,
-                                  float2* mats, int n_mat, int32_t* angles, int n_ang, double* slot_scale,
-                                  int n_slots, const QfFrame* frame_in, QfFrame* frame_out) {
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= rows) return;
+__device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adjoint, int row, float2* M,
+                               int32_t* angles, int n_ang, double* slot_scale, int n_slots,
+                               const QfFrame* frame_in, QfFrame* frame_out) {
   uint32_t x = 0, z = 0;
   double m = 1.0;
   if (frame_in) {
@@ -421,7 +419,6 @@ __global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int 
     z = frame_in[row].z;
     m = frame_in[row].m;
   }
-  float2* M = mats + (size_t)row * n_mat;
   for (int e = 0; e < n_ev; ++e) {
     const int32_t* E = ev + (size_t)e * 8;
     const int kind = E[0], q0 = E[1], q1 = E[2], off = E[3], slot = E[4], col = E[5];
@@ -534,6 +531,37 @@ __global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int 
     }
   }
   if (frame_out) frame_out[row] = QfFrame{x, z, m};
+}
+
+// One CTA per row: the row's matrix slab and the event list are staged in shared memory,
+// one thread walks the events (shared-memory latency instead of a global round trip per
+// event), the CTA writes the slab back.
+__global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int adjoint, int rows,
+                                  float2* mats, int n_mat, int32_t* angles, int n_ang, double* slot_scale,
+                                  int n_slots, const QfFrame* frame_in, QfFrame* frame_out) {
+  extern __shared__ __align__(16) unsigned char fw_smem[];
+  float2* Ms = reinterpret_cast<float2*>(fw_smem);
+  int32_t* Es = reinterpret_cast<int32_t*>(Ms + n_mat);
+  const int row = blockIdx.x;
+  float2* M = mats + (size_t)row * n_mat;
+  for (int i = threadIdx.x; i < n_mat; i += blockDim.x) Ms[i] = M[i];
+  for (int i = threadIdx.x; i < n_ev * 8; i += blockDim.x) Es[i] = ev[i];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    frame_walk_row(Es, n_ev, adjoint, row, Ms, angles, n_ang, slot_scale, n_slots, frame_in, frame_out);
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_mat; i += blockDim.x) M[i] = Ms[i];
+}
+
+// Fallback for slabs too large for shared memory: one thread per row on global memory.
+__global__ void frame_walk_global_kernel(const int32_t* __restrict__ ev, int n_ev, int adjoint, int rows,
+                                         float2* mats, int n_mat, int32_t* angles, int n_ang,
+                                         double* slot_scale, int n_slots, const QfFrame* frame_in,
+                                         QfFrame* frame_out) {
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  frame_walk_row(ev, n_ev, adjoint, row, mats + (size_t)row * n_mat, angles, n_ang, slot_scale, n_slots,
+                 frame_in, frame_out);
 }
 
 }  // namespace qf
@@ -651,11 +679,23 @@ int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, fl
                   int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
                   QfFrame* frame_out, void* stream) {
   if (rows == 0) return 0;
+  const size_t smem = (size_t)n_mat * sizeof(float2) + (size_t)n_events * 8 * sizeof(int32_t);
+  if (smem <= 96 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(frame_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      configured = true;
+    }
+    frame_walk_kernel<<<rows, 128, smem, (cudaStream_t)stream>>>(
+        events, n_events, adjoint, rows, reinterpret_cast<float2*>(mats), n_mat, angles, n_ang, slot_scale,
+        n_slots, frame_in, frame_out);
+    return check_launch("frame_walk_kernel");
+  }
   const int T = 128;
-  frame_walk_kernel<<<(rows + T - 1) / T, T, 0, (cudaStream_t)stream>>>(
+  frame_walk_global_kernel<<<(rows + T - 1) / T, T, 0, (cudaStream_t)stream>>>(
       events, n_events, adjoint, rows, reinterpret_cast<float2*>(mats), n_mat, angles, n_ang, slot_scale, n_slots,
       frame_in, frame_out);
-  return check_launch("frame_walk_kernel");
+  return check_launch("frame_walk_global_kernel");
 }
 
 int qf_pauli_expect(const float* psi, int n, int rows, int n_terms, const uint32_t* xmask, const uint32_t* zmask,
