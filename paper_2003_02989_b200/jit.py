@@ -44,7 +44,10 @@ class QfJitArgs(C.Structure):
 
 
 GS_THREAD_BYTES = 40 * 1024
-PERSIST = os.environ.get("QF_PERSIST", "0") not in ("0", "", "false", "no")   # measured slower (no prefetch)
+# 0: one CTA per tile; 1: persistent CTAs (measured slower); 2: persistent CTAs that prefetch
+# the next tile into shared memory with cp.async while computing the current one
+PERSIST_MODE = int(os.environ.get("QF_PERSIST", "0") or 0)
+PERSIST = PERSIST_MODE > 0
 
 
 def _flit(x: float) -> str:
@@ -175,6 +178,14 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                 int_tables[k_] = (ip, tbl_bytes)
                 tbl_bytes += (2 * ip[2] + 1) * 16
         smem = (smem + 15) // 16 * 16 + tbl_bytes
+        prefetch = PERSIST_MODE == 2 and init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI)
+        NPF = (2 if (adj and init == pl.INIT_LOAD) else 1) if prefetch else 0
+        pf_off = smem
+        smem += NPF * TILE * 8
+        tileq = [q for q in range(n) if q not in set(outer)]
+
+        def dep(l):
+            return sum(((l >> i) & 1) << tileq[i] for i in range(L))
         pass_ops = [prog.ops[k] for s_ in range(sb, se) for k in range(int(prog.stages[s_][48]),
                                                                         int(prog.stages[s_][49]))]
         heavy = any(int(op_[0]) == pl.OP_DENSE2 or (int(op_[0]) == pl.OP_DENSE1 and int(op_[9]) == pl.CLS_GENERAL)
@@ -197,7 +208,9 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         w(f"  float* CO = reinterpret_cast<float*>(ANG + {acnt});")
         w(f"  float* GS = CO + {ccnt};")
         if int_tables:
-            w(f"  float4* TB = reinterpret_cast<float4*>(smem_raw + {(smem - tbl_bytes)});")
+            w(f"  float4* TB = reinterpret_cast<float4*>(smem_raw + {(pf_off - tbl_bytes)});")
+        if prefetch:
+            w(f"  float2* PF = reinterpret_cast<float2*>(smem_raw + {pf_off});")
         w("  const u32 t = threadIdx.x;")
         if PERSIST:
             # persistent CTAs: a contiguous run of tiles each, so the row's staged matrices,
@@ -210,6 +223,24 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
             w(f"  float2 v0[{NR}];")
             if adj:
                 w(f"  float2 v1[{NR}];")
+            if prefetch:
+                # chunk c (16 B = local amplitudes 2c, 2c+1) of thread t: c = t + k * NT
+                K = (TILE // 2) // NT
+                dt = _xor_expr([dep(2 << i) for i in range(TB)])
+                w(f"  const u32 pfd = {dt};")
+                w("  auto prefetch = [&](u32 nt) {")
+                w(f"    const u32 nrow = nt >> {n - L}, no = nt & {(1 << (n - L)) - 1}u;")
+                nb = " | ".join(f"(((no >> {i}) & 1u) << {q})" for i, q in enumerate(outer)) or "0u"
+                w(f"    const u32 nbase = {nb};")
+                arrays = [("a.psi", 0)] + ([("a.lam", TILE)] if NPF == 2 else [])
+                for arr, soff in arrays:
+                    w(f"    {{ const float2* __restrict__ src = {arr} + ((size_t)nrow << {n}) + (nbase | pfd);")
+                    for k in range(K):
+                        w(f"      cp_async16(PF + {soff + 2 * k * NT} + 2 * t, src + {dep(2 * k * NT)}ll);")
+                    w("    }")
+                w("    cp_async_commit();")
+                w("  };")
+                w("  if (tile < tend) prefetch(tile);")
             w("  for (; tile < tend; ++tile) {")
             w(f"  const int row = (int)(tile >> {n - L});")
             w(f"  const u32 o = tile & {(1 << (n - L)) - 1}u;")
@@ -276,7 +307,26 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         # ---- load / init ----
         st0 = st_rows[0]
         w(f"  const u32 gt0 = base | {_xor_expr(tglob(st0))};")
-        if init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI):
+        if prefetch:
+            # this tile landed in PF (natural local order) during the previous tile
+            def lidx(qs):
+                return [1 << tileq.index(q) for q in qs]
+            tl = _xor_expr(lidx([int(st0[8 + i]) for i in range(TB)]))
+            w("  cp_async_wait_all();")
+            w("  __syncthreads();")
+            w(f"  {{ const u32 tl0 = {tl};")
+            for r in range(NR):
+                lo = 0
+                for j in range(R):
+                    if r >> j & 1:
+                        lo |= 1 << tileq.index(int(st0[j]))
+                w(f"    v0[{r}] = PF[tl0 ^ {lo}u];")
+                if adj:
+                    w(f"    v1[{r}] = " + (f"PF[{TILE} + (tl0 ^ {lo}u)];" if NPF == 2 else "make_float2(0.f, 0.f);"))
+            w("  }")
+            w("  __syncthreads();")
+            w("  if (tile + 1 < tend) prefetch(tile + 1);")
+        elif init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI):
             # pointer + 64-bit constant offsets: u32 index sums above 2^29 elements were
             # miscompiled (half-width loads) by nvcc/NVRTC 12.9 at n >= 30
             w("  const float2* __restrict__ pt0 = psi + gt0;")
