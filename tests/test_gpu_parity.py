@@ -448,3 +448,60 @@ def test_batched_parameter_shift_matches_reference_ps(cuda, golden):
     for b in range(3):
         bind = dict(zip(syms, th[b].astype(np.float64)))
         _close_grad(g2[b], orc.parameter_shift_grad(c2, o2, bind)[0])
+
+
+# ---------------------------------------------------------------------------
+# determinism, re-entrancy and statistical bands (ref test_sim.py:250-334,
+# test_bench_cli.py:206-214, test_gradients.py:275-325)
+# ---------------------------------------------------------------------------
+
+
+def test_concurrent_calls_are_deterministic(cuda):
+    """The engine is re-entrant: calls from several threads give the serial results
+    bit-for-bit (the reference's bench runs simulate from worker threads)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(71)
+    c = random_circuit(rng, 12, 120, n_sym=4)
+    syms = circuit_symbols(c)
+    theta = rng.uniform(-2, 2, size=(6, len(syms))).astype(np.float32)
+    obs = [random_observable(rng, 12, diag=True), random_observable(rng, 12)]
+    want_e, want_g = ops.expectation_and_gradient([c] * 6, syms, theta, obs)
+    want_s = sim.simulate(resolve(c, dict(zip(syms, theta[0].astype(np.float64))))).amplitudes
+
+    def job(i):
+        if i % 2:
+            return ops.expectation_and_gradient([c] * 6, syms, theta, obs)
+        return sim.simulate(resolve(c, dict(zip(syms, theta[0].astype(np.float64))))).amplitudes
+
+    with ThreadPoolExecutor(4) as ex:
+        outs = list(ex.map(job, range(8)))
+    for i, o in enumerate(outs):
+        if i % 2:
+            np.testing.assert_array_equal(o[0], want_e)
+            np.testing.assert_array_equal(o[1], want_g)
+        else:
+            np.testing.assert_array_equal(o, want_s)
+
+
+def test_sampling_statistics_and_seed_determinism(cuda):
+    c = Circuit(3, [G.h(0), G.x(2)])
+    a = sim.sample(sim.simulate(c), 40000, seed=9)
+    b = sim.sample(sim.simulate(c), 40000, seed=9)
+    d = sim.sample(sim.simulate(c), 40000, seed=10)
+    bits = np.asarray(a.bitstrings)
+    np.testing.assert_array_equal(bits, np.asarray(b.bitstrings))
+    assert not np.array_equal(bits, np.asarray(d.bitstrings))
+    assert abs(bits[:, 0].mean() - 0.5) < 0.01          # binomial band (ref test_sim.py:259-271)
+    assert bits[:, 1].sum() == 0 and bits[:, 2].min() == 1
+
+
+def test_sampled_expectation_band_over_seeds(cuda):
+    """Mean of sampled <Z0 + X1> over seeds within 5 sigma of the exact value (ref
+    test_sim.py:318-334)."""
+    c = Circuit(2, [G.ry(0.7, 0), G.rx(0.4, 1), G.h(1), G.cz(0, 1), G.h(1)])
+    obs = PauliSum([PauliString(1.0, {0: "Z"}), PauliString(1.0, {1: "X"})])
+    exact = sim.expectation(sim.simulate(c), obs)
+    vals = np.array([sim.sampled_expectation(c, obs, 200, seed=s) for s in range(100)])
+    sigma = np.sqrt(2.0 / 200 / 100)
+    assert abs(vals.mean() - exact) < 5 * sigma

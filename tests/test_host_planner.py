@@ -119,3 +119,40 @@ def test_planner_qcnn_and_brickwork_emulated():
     _check_program(full, PauliSum([PauliString(1.0, {7: "Z"})]), 10, theta)
     bw = wl.brickwork_circuit(12, 5, seed=3)
     _check_program(bw, wl.z_sum(12), 12, np.zeros((1, 0)))
+
+
+@pytest.mark.parametrize("adjoint", [False, True])
+def test_frame_programs_event_invariants(adjoint):
+    """Pauli-frame programs (planner.build_program(frame=True)): one frame event per dense /
+    diagonal / observable op, in execution order, with matching classes and x-mask columns."""
+    from circuits import random_circuit
+    from paper_2003_02989_b200.engine import _Term, _TermList
+
+    rng = np.random.default_rng(17 + adjoint)
+    c = random_circuit(rng, 11, 160, n_sym=4)
+    syms = circuit_symbols(c)
+    si = {s: i for i, s in enumerate(syms)}
+    obs = _TermList([_Term({0: "Z", 3: "Z"}, 1.0), _Term({5: "Z"}, 0.5)])
+    if adjoint:
+        prog = pl.build_program(c, pl.analyse(c, si), 11, adjoint=True, observables=[obs], lam_diag=True, frame=True)
+    else:
+        prog = pl.build_program(c, pl.analyse(c, si), 11, adjoint=False, observables=[obs], obs_diag_ids=[0],
+                                frame=True)
+    assert prog.frame
+    ev = prog.frame_events
+    kinds = {pl.OP_DENSE1: {pl.EV_NX, pl.EV_NY, pl.EV_ABS1}, pl.OP_DENSE2: {pl.EV_ABS2, pl.EV_NP},
+             pl.OP_DIAG: {pl.EV_DIAG}, pl.OP_OBS: {pl.EV_OBS}}
+    assert len(ev) == len(prog.ops)
+    for op, e in zip(prog.ops, ev):
+        k, cls = int(op[0]), int(op[9])
+        assert int(e[0]) in kinds[k]
+        if k in (pl.OP_DENSE1, pl.OP_DENSE2):
+            assert int(e[3]) == int(op[3])                   # the op's matrix slab
+            assert int(e[4]) == int(op[7])                   # its gradient slot
+            assert (int(e[0]) in (pl.EV_NX, pl.EV_NY, pl.EV_NP)) == (cls in (pl.CLS_NX, pl.CLS_NY, pl.CLS_NP))
+            assert cls != pl.CLS_XLIKE                        # absorbed X frames would break it
+        else:
+            assert int(op[11]) >= 0 and int(e[5]) == int(op[11])
+            assert prog.recipe["term_src"].reshape(-1, 2)[int(op[11])][0] == 2
+    if adjoint:
+        assert any(int(e[0]) == pl.EV_NP for e in ev)        # pauli_pair_pow X/Y couplings
