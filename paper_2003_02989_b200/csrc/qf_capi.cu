@@ -189,7 +189,7 @@ __global__ void pauli_expect_kernel(const float2* __restrict__ psi, int n, int n
   extern __shared__ double tacc[];
   const int row = blockIdx.y, chunk = blockIdx.x;
   const float2* p = psi + ((size_t)row << n);
-  for (int k = threadIdx.x; k < n_terms; k += blockDim.x) tacc[k] = 0.0;
+  const int nw = blockDim.x >> 5;  // per-(term, warp) partials summed in warp order: deterministic
   __syncthreads();
   const uint32_t x0 = (uint32_t)chunk * kExpectChunk;
   const uint32_t len = min((uint32_t)kExpectChunk, (uint32_t)1u << n);
@@ -206,11 +206,14 @@ __global__ void pauli_expect_kernel(const float2* __restrict__ psi, int n, int n
       acc += (__popc(x & z) & 1) ? -v : v;
     }
     const double ad = warp_sum_d((double)acc);
-    if ((threadIdx.x & 31) == 0) atomicAdd(tacc + k, ad);
+    if ((threadIdx.x & 31) == 0) tacc[k * nw + (threadIdx.x >> 5)] = ad;
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < n_terms; k += blockDim.x)
-    partials[((size_t)row * n_terms + k) * chunks + chunk] = tacc[k] * (double)coefs[row * cstride + k];
+  for (int k = threadIdx.x; k < n_terms; k += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += tacc[k * nw + w];
+    partials[((size_t)row * n_terms + k) * chunks + chunk] = s * (double)coefs[row * cstride + k];
+  }
 }
 
 __global__ void pauli_apply_kernel(const float2* __restrict__ psi, float2* __restrict__ lam, int n, int n_terms,
@@ -707,7 +710,7 @@ int qf_pauli_expect(const float* psi, int n, int rows, int n_terms, const uint32
   }
   const int chunks = (int)(((int64_t)1 << n) + kExpectChunk - 1) / kExpectChunk;
   dim3 grid(chunks, rows);
-  pauli_expect_kernel<<<grid, 256, n_terms * sizeof(double), (cudaStream_t)stream>>>(
+  pauli_expect_kernel<<<grid, 256, n_terms * 8 * sizeof(double), (cudaStream_t)stream>>>(
       reinterpret_cast<const float2*>(psi), n, n_terms, xmask, zmask, ny, coefs, coef_stride, partials, chunks);
   return check_launch("pauli_expect_kernel");
 }

@@ -295,8 +295,11 @@ __global__ void __launch_bounds__(KTraits<L, R, ADJ>::NT, KTraits<L, R, ADJ>::MI
   float2* tile = reinterpret_cast<float2*>(smem_raw);
   QfStage* sst = reinterpret_cast<QfStage*>(tile + NA * TILE);
   QfOp* sop = reinterpret_cast<QfOp*>(sst + st_cnt);
+  // slot partials: one entry per (slot, warp), summed in warp order at the end, so results
+  // are bit-identical from call to call (no shared-memory atomics)
+  constexpr int NW = NT / 32;
   double* ssm = reinterpret_cast<double*>(sop + op_cnt);
-  float2* msm = reinterpret_cast<float2*>(ssm + slot_cnt);
+  float2* msm = reinterpret_cast<float2*>(ssm + slot_cnt * NW);
   uint2* stm = reinterpret_cast<uint2*>(msm + mat_cnt);
   float* stw = reinterpret_cast<float*>(stm + term_cnt);
   int32_t* sgr = reinterpret_cast<int32_t*>(stw + (ADJ ? term_cnt : 0));
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(KTraits<L, R, ADJ>::NT, KTraits<L, R, ADJ>::MI
     s32 = reinterpret_cast<const int32_t*>(P.ops + op_begin);
     d32 = reinterpret_cast<int32_t*>(sop);
     for (int i = t; i < op_cnt * 16; i += NT) d32[i] = s32[i];
-    for (int i = t; i < slot_cnt; i += NT) ssm[i] = 0.0;
+    for (int i = t; i < slot_cnt * NW; i += NT) ssm[i] = 0.0;
     const float2* src = a.mats + (size_t)row * P.n_mat + mat_begin;
     for (int i = t; i < mat_cnt; i += NT) msm[i] = src[i];
     const int32_t* arow = a.angles + (size_t)row * P.n_ang;
@@ -418,7 +421,7 @@ __global__ void __launch_bounds__(KTraits<L, R, ADJ>::NT, KTraits<L, R, ADJ>::MI
             });
             if (gk != 0) gacc *= g[4].x;
             const double gs = warp_sum_d((double)gacc);
-            if ((t & 31) == 0) atomicAdd(ssm + (op.slot - slot_begin), gs);
+            if ((t & 31) == 0) ssm[(op.slot - slot_begin) * NW + (t >> 5)] += gs;
           }
         }
         dispatch1<R>(op.s0, [&]<int J>() {
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(KTraits<L, R, ADJ>::NT, KTraits<L, R, ADJ>::MI
             float gacc = 0.f;
             dispatch2<R>(op.s0, op.s1, [&]<int J0, int J1>() { gacc = grad2<J0, J1, NR>(v[0], v[1], g); });
             const double gs = warp_sum_d((double)gacc);
-            if ((t & 31) == 0) atomicAdd(ssm + (op.slot - slot_begin), gs);
+            if ((t & 31) == 0) ssm[(op.slot - slot_begin) * NW + (t >> 5)] += gs;
           }
           dispatch2<R>(op.s0, op.s1, [&]<int J0, int J1>() {
             apply2<J0, J1, NR>(v[0], u, true);
@@ -460,7 +463,7 @@ __global__ void __launch_bounds__(KTraits<L, R, ADJ>::NT, KTraits<L, R, ADJ>::MI
 #pragma unroll
             for (int r = 0; r < NR; ++r) acc = fmaf(W[r], w[r], acc);
             const double as = warp_sum_d((double)acc);
-            if ((t & 31) == 0) atomicAdd(ssm + (op.slot - slot_begin), as);
+            if ((t & 31) == 0) ssm[(op.slot - slot_begin) * NW + (t >> 5)] += as;
           }
         }
         uint32_t A[NR];
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(KTraits<L, R, ADJ>::NT, KTraits<L, R, ADJ>::MI
         }
         if (op.slot >= 0) {
           const double es = warp_sum_d((double)e);
-          if ((t & 31) == 0) atomicAdd(ssm + (op.slot - slot_begin), es);
+          if ((t & 31) == 0) ssm[(op.slot - slot_begin) * NW + (t >> 5)] += es;
         }
       }
     }
@@ -509,8 +512,11 @@ __global__ void __launch_bounds__(KTraits<L, R, ADJ>::NT, KTraits<L, R, ADJ>::MI
   if (slot_cnt > 0) {
     __syncthreads();
     const int tiles = 1 << tiles_log2;
-    for (int i = t; i < slot_cnt; i += NT)
-      a.partials[((size_t)row * P.n_slots + slot_begin + i) * tiles + o] = ssm[i];
+    for (int i = t; i < slot_cnt; i += NT) {
+      double acc = 0.0;
+      for (int w = 0; w < NW; ++w) acc += ssm[i * NW + w];
+      a.partials[((size_t)row * P.n_slots + slot_begin + i) * tiles + o] = acc;
+    }
   }
 }
 
@@ -524,7 +530,7 @@ static int launch_pass(const PassArgs& a, const QfPass& hp, cudaStream_t stream)
   constexpr int NA = ADJ ? 2 : 1;
   const size_t terms = (size_t)(hp.term_end - hp.term_begin);
   size_t smem = (size_t)NA * (1u << L) * sizeof(float2) + (size_t)(hp.stage_end - hp.stage_begin) * sizeof(QfStage) +
-                (size_t)(hp.op_end - hp.op_begin) * sizeof(QfOp) + (size_t)(hp.slot_end - hp.slot_begin) * 8 +
+                (size_t)(hp.op_end - hp.op_begin) * sizeof(QfOp) + (size_t)(hp.slot_end - hp.slot_begin) * 8 * (NT / 32) +
                 (size_t)(hp.mat_end - hp.mat_begin) * sizeof(float2) + terms * 8 + (ADJ ? terms * 4 : 0) +
                 (size_t)(hp.grp_end - hp.grp_begin) * 4;
   static bool configured = false;

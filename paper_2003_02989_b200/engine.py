@@ -367,7 +367,9 @@ class Bound:
             up = torch.as_tensor(upstream, dtype=torch.float64).to(dev).reshape(B, -1)
             if up.shape[1] != self.n_obs:
                 raise ValueError(f"upstream shape {tuple(up.shape)} != ({B}, {self.n_obs})")
-        hw_t = (up @ self.hmix).to(torch.float32).contiguous()
+        # elementwise product + fixed-order sum: bit-identical across calls and threads (a
+        # cuBLAS GEMM may pick different reduction orders)
+        hw_t = (up[:, :, None] * self.hmix[None, :, :]).sum(dim=1).to(torch.float32).contiguous()
         mats = torch.empty((B, max(ad.prog.n_mat, 1)), dtype=torch.complex64, device=dev)
         angs = torch.empty((B, max(ad.prog.n_ang, 1)), dtype=torch.int32, device=dev)
         rec = ad.recipe(self.fixed_a, self.fixed_a_rows, self.const_a, self.const_a_rows)
