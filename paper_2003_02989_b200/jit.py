@@ -43,7 +43,7 @@ class QfJitArgs(C.Structure):
                 ("coef_stride", C.c_int), ("n_slots", C.c_int), ("tiles_log2", C.c_int), ("pad", C.c_int)]
 
 
-GS_THREAD_BYTES = 40 * 1024
+GS_THREAD_BYTES = int(os.environ.get("QF_GS_BYTES", str(40 * 1024)))
 # 0: one CTA per tile; 1: persistent CTAs (measured slower); 2: persistent CTAs that prefetch
 # the next tile into shared memory with cp.async while computing the current one
 PERSIST_MODE = int(os.environ.get("QF_PERSIST", "0") or 0)
