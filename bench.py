@@ -285,9 +285,8 @@ def run_gpu(args, rank, world):
     kname = (f"plan-specialised NVRTC tile-pass kernels qf_f_p*/qf_a_p* (forward L{fw.prog.L}/R{fw.prog.R}, "
              f"adjoint L{ad.prog.L}/R{ad.prog.R}, Pauli-frame normalised={bool(fw.frame)})"
              if jf is not None else "qf::pass_kernel (interpreted)")
-    reps = 3
-    times_f = np.zeros(len(fb))
-    times_a = np.zeros(len(ab))
+    reps = 5
+    samp_f, samp_a = [], []
     for r in range(reps + 1):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(fb) + len(ab) + 1)]
         ev[0].record(stream)
@@ -310,10 +309,11 @@ def run_gpu(args, rank, world):
         torch.cuda.synchronize(dev)
         if r == 0:
             continue  # warm-up round
-        for p in range(len(fb)):
-            times_f[p] += ev[p].elapsed_time(ev[p + 1]) / reps
-        for p in range(len(ab)):
-            times_a[p] += ev[len(fb) + p].elapsed_time(ev[len(fb) + p + 1]) / reps
+        samp_f.append([ev[p].elapsed_time(ev[p + 1]) for p in range(len(fb))])
+        samp_a.append([ev[len(fb) + p].elapsed_time(ev[len(fb) + p + 1]) for p in range(len(ab))])
+    # per-pass median over the repetitions (a single hiccup must not skew the roofline)
+    times_f = np.median(np.array(samp_f), axis=0)
+    times_a = np.median(np.array(samp_a), axis=0)
     peak, peak_kind = _peaks()
     tot_bytes = sum(fb) + sum(ab)
     tot_ms = times_f.sum() + times_a.sum()

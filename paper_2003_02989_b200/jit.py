@@ -136,7 +136,10 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
     NA = 2 if adj else 1
     TILE = 1 << L
     env_minb = int(os.environ.get("QF_MINB_ADJ" if adj else "QF_MINB_FWD", "0"))
-    minb = env_minb or max(1, min(8, 65536 // (NT * (NR * 2 * NA + 32))))
+    # measured best (tools/sweep.sh): 128 registers for the 12/5 forward (4 CTAs x 128
+    # threads), 64 for the 12/4 forward, 128 for the 12/4 adjoint (2 CTAs x 256 threads)
+    tuned = {(12, 5, False): 4, (12, 4, False): 4, (12, 4, True): 2}.get((L, R, adj))
+    minb = env_minb or tuned or max(1, min(8, 65536 // (NT * (NR * 2 * NA + 32))))
     gm = prog.genmats.reshape(-1, 2) if len(prog.genmats) else np.zeros((0, 2), np.float32)
     src = []
     names, geo = [], []
@@ -190,7 +193,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                                                                         int(prog.stages[s_][49]))]
         heavy = any(int(op_[0]) == pl.OP_DENSE2 or (int(op_[0]) == pl.OP_DENSE1 and int(op_[9]) == pl.CLS_GENERAL)
                     for op_ in pass_ops)
-        minb_p = min(minb, 2) if (heavy and not env_minb) else minb
+        minb_p = min(minb, max(1, 65536 // (NT * 128))) if (heavy and not env_minb) else minb
 
         def gs_store(slot_rel, expr):
             if per_thread_gs:

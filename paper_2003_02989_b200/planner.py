@@ -31,7 +31,7 @@ from .pauli import term_masks
 
 N_MIN = 10          # smaller registers are padded (extra qubits stay |0>)
 LANE_Q = 4          # qubits 0..3 are always lane bits at load/store (128-byte runs)
-FWD_L, FWD_R = 12, 4   # 4 CTAs/SM at 64 registers: measured faster than 13/5 at 2 CTAs/SM
+FWD_L, FWD_R = 12, 5   # 4 CTAs/SM x 128 threads at 128 registers: fastest measured (tools/sweep.sh)
 ADJ_L, ADJ_R = 12, 4
 
 
@@ -764,9 +764,15 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     and the per-row frame (x, z, m) is tracked by the build step in execution order:
     general dense ops absorb the frame into their matrix, diagonal ops / observables are
     evaluated at index ^ x, and slot sums are scaled by m (and the generator's sign)."""
-    L, R = geometry(adjoint)
-    L = min(L, n)
     ops = build_ops(infos, adjoint)
+    L, R = geometry(adjoint)
+    if not adjoint and R == 5 and "QF_GEOM_FWD" not in __import__("os").environ:
+        # dense two-qubit blocks hold 16 matrix pairs in registers: with 32 amplitudes per
+        # thread they spill, so programs with many of them use 16 amplitudes per thread
+        n2 = sum(o.kind == OP_DENSE2 for o in ops)
+        if n2 * 10 > len(ops):
+            L, R = 12, 4
+    L = min(L, n)
     frame = frame and frame_eligible(ops, infos, adjoint)
     if from_state and not adjoint:
         init = {}
