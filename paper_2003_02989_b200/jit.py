@@ -160,7 +160,8 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         # shuffle reduction, so the CTA keeps its occupancy
         per_thread_gs = scnt * NT * 4 <= GS_THREAD_BYTES
         GSW = NT if per_thread_gs else NT // 32
-        smem = NA * TILE * 8 + mcnt * 16 + acnt * 4 + ccnt * 4 + scnt * GSW * 4 + 16
+        ws_floats = (NT // 32) * 32 if (scnt and per_thread_gs) else 0
+        smem = NA * TILE * 8 + mcnt * 16 + acnt * 4 + ccnt * 4 + scnt * GSW * 4 + ws_floats * 4 + 16
         # integer-weight phase polynomials (full-WHT path only) get a per-CTA phase table
         int_tables = {}
         tbl_bytes = 0
@@ -210,6 +211,8 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         w(f"  int* ANG = reinterpret_cast<int*>(MN + {mcnt});")
         w(f"  float* CO = reinterpret_cast<float*>(ANG + {acnt});")
         w(f"  float* GS = CO + {ccnt};")
+        if ws_floats:
+            w(f"  float* WS = GS + {scnt * GSW};")
         if int_tables:
             w(f"  float4* TB = reinterpret_cast<float4*>(smem_raw + {(pf_off - tbl_bytes)});")
         if prefetch:
@@ -598,7 +601,25 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                 if adj:
                     w(f"    lts[{roff(stl, r)}ll] = v1[{r}];")
             w("  }")
-        if scnt:
+        if scnt and per_thread_gs and NT >= 64:
+            # each thread's slot values are its own GS entries: per 32-slot chunk, a warp
+            # transpose-reduction leaves slot L's warp sum on lane L; warps combine in order
+            NWP = NT // 32
+            for c0 in range(0, scnt, 32):
+                K = min(32, scnt - c0)
+                w("  {")
+                w("    float x[32];")
+                for i in range(32):
+                    w(f"    x[{i}] = {f'GS[{(c0 + i) * NT} + t]' if i < K else '0.f'};")
+                w("    warp_transpose_sum32(x, t & 31u);")
+                w("    __syncthreads();")
+                w(f"    WS[(t >> 5) * 32 + (t & 31)] = x[0];")
+                w("    __syncthreads();")
+                w(f"    if (t < {K}) {{ double acc = 0.0;")
+                w(f"      for (int wv = 0; wv < {NWP}; ++wv) acc += (double)WS[wv * 32 + t];")
+                w(f"      a.partials[((size_t)row * a.n_slots + {slb + c0} + t) * {1 << (n - L)} + o] = acc; }}")
+                w("  }")
+        elif scnt:
             w("  __syncthreads();")
             w(f"  for (int s = t >> 5; s < {scnt}; s += {max(NT // 32, 1)}) {{")
             w("    double acc = 0.0;")
@@ -625,8 +646,15 @@ def _cache_dir() -> str:
 
 
 def compile_kernel(source: str, name: str) -> bytes:
-    """NVRTC-compile one kernel (prelude + body) to an sm_100a cubin, with a disk cache."""
+    """NVRTC-compile one kernel (prelude + body) to an sm_100a cubin, with a disk cache.
+    QF_JIT_DUMP=dir writes the source as dir/<name>.cu (ncu --import-source resolves the
+    -lineinfo file name relative to the working directory)."""
     full = prelude() + "\n" + source
+    dump = os.environ.get("QF_JIT_DUMP")
+    if dump:
+        os.makedirs(dump, exist_ok=True)
+        with open(os.path.join(dump, name + ".cu"), "w") as f:
+            f.write(full)
     key = hashlib.sha256(full.encode() + b"|".join(_OPTS)).hexdigest()
     path = os.path.join(_cache_dir(), key + ".cubin")
     if os.path.exists(path):
