@@ -637,6 +637,8 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
 
 
 _OPTS = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", b"--device-as-default-execution-space"]
+if os.environ.get("QF_GRAD_CHAINS"):
+    _OPTS.append(f"-DGRAD_CHAINS={int(os.environ['QF_GRAD_CHAINS'])}".encode())
 
 
 def _cache_dir() -> str:
