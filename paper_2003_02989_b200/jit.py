@@ -256,6 +256,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         else:
             w(f"  const int row = (int)(blockIdx.x >> {n - L});")
             w(f"  const u32 o = blockIdx.x & {(1 << (n - L)) - 1}u;")
+        mark_stage = len(o)
         if mcnt:
             # stage the row's matrices: as built for the forward sweep; conjugate-transposed
             # (U^dag) for general / X-like / real dense ops of the adjoint sweep
@@ -289,11 +290,13 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
             w("  __syncthreads();")
         if PERSIST:
             w("  }")
+        mark_ptr = len(o)
         base = " | ".join(f"(((o >> {i}) & 1u) << {q})" for i, q in enumerate(outer)) or "0u"
         w(f"  const u32 base = {base};")
         w(f"  float2* __restrict__ psi = a.psi + ((size_t)row << {n});")
         if adj:
             w(f"  float2* __restrict__ lam = a.lam + ((size_t)row << {n});")
+        mark_ptr_end = len(o)
 
         st_rows = [prog.stages[s] for s in range(sb, se)]
 
@@ -311,6 +314,7 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
             return x
 
         # ---- load / init ----
+        mark_load = len(o)
         st0 = st_rows[0]
         w(f"  const u32 gt0 = base | {_xor_expr(tglob(st0))};")
         if prefetch:
@@ -368,6 +372,15 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                     w(f"    v0[{r | (1 << j)}] = cmul(v0[{r}], f1); v0[{r}] = cmul(v0[{r}], f0);")
                 w("  }")
 
+        mark_load_end = len(o)
+        if not PERSIST and not prefetch and not adj and init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI):
+            # (forward sweep only: measured slower for the adjoint)
+            # issue the tile's global loads before staging the row's matrices / tables, so
+            # the staging latency (loads, syncs, table sincos) hides behind the tile loads
+            vdecl = [ln for ln in o[mark_stage:mark_ptr] if ln.startswith("  float2 v0[") or
+                     ln.startswith("  float2 v1[")]
+            staging = [ln for ln in o[mark_stage:mark_ptr] if ln not in vdecl]
+            o[mark_stage:mark_load_end] = (vdecl + o[mark_ptr:mark_ptr_end] + o[mark_load:mark_load_end] + staging)
         # ---- stages ----
         for si, st in enumerate(st_rows):
             if si:
