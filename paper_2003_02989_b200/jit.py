@@ -43,6 +43,7 @@ class QfJitArgs(C.Structure):
                 ("coef_stride", C.c_int), ("n_slots", C.c_int), ("tiles_log2", C.c_int), ("pad", C.c_int)]
 
 
+FUSED_GRAD = os.environ.get("QF_FUSED_GRAD", "0") not in ("0", "", "false")   # measured 2% slower
 GS_THREAD_BYTES = int(os.environ.get("QF_GS_BYTES", str(40 * 1024)))
 # 0: one CTA per tile; 1: persistent CTAs (measured slower); 2: persistent CTAs that prefetch
 # the next tile into shared memory with cp.async while computing the current one
@@ -415,6 +416,12 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
                     # Pauli-frame normalised rotation: the build step wrote tau (adjoint-ready)
                     ax = 1 if cls == pl.CLS_NX else 2
                     w(f"    {{ const float tau = M[{moff}].x;")
+                    if adj and slot >= 0 and FUSED_GRAD:
+                        g0 = int(op[8])
+                        sc = float(gm[g0 + 4, 0])
+                        w("      " + gs_store(slot - slb, f"{_flit(sc)} * gradApplyN<{s0}, {NR}, {gk}, {ax}>(v0, v1, tau)"))
+                        w("    }")
+                        continue
                     if adj and slot >= 0:
                         g0 = int(op[8])
                         sc = float(gm[g0 + 4, 0])
