@@ -316,6 +316,19 @@ class LoopbackExchange:
     def allreduce_sum(self, x):
         return x.sum(dim=0, keepdim=True)
 
+    def remote_targets(self, psi):
+        """Receive shards for a swap fused into the preceding pass: (peer pointer array on the
+        device, rank of row 0, receive tensor)."""
+        import torch
+
+        recv = torch.empty_like(psi)
+        ptrs = torch.tensor([recv[r].data_ptr() for r in range(recv.shape[0])], dtype=torch.int64,
+                            device=psi.device)
+        return ptrs, 0, recv
+
+    def remote_done(self):
+        pass
+
 
 class NcclExchange:
     """One process per GPU: rank r owns shard r; swaps are one all_to_all_single
@@ -332,6 +345,7 @@ class NcclExchange:
         self.g = g
         self.ranks = [dist.get_rank(group)]
         self._spare = None
+        self._symm = None
 
     def swap(self, psi, n_loc: int):
         if self._spare is None or self._spare.shape != psi.shape:
@@ -344,6 +358,30 @@ class NcclExchange:
     def allreduce_sum(self, x):
         self.dist.all_reduce(x, group=self.group)
         return x
+
+    def remote_targets(self, psi):
+        """Fused swaps need every rank's receive shard mapped into this process (NVLink peer
+        memory): torch symmetric memory when available, else None (plain all-to-all)."""
+        try:
+            import torch
+            import torch.distributed._symmetric_memory as symm
+        except Exception:
+            return None
+        try:
+            if self._symm is None or self._symm[0].shape != psi.shape:
+                buf = symm.empty(psi.shape, dtype=psi.dtype, device=psi.device)
+                hdl = symm.rendezvous(buf, self.dist.group.WORLD if self.group is None else self.group)
+                ptrs = torch.tensor([int(p) for p in hdl.buffer_ptrs], dtype=torch.int64, device=psi.device)
+                self._symm = (buf, hdl, ptrs)
+        except Exception:
+            return None
+        buf, hdl, ptrs = self._symm
+        self._symm_hdl = hdl
+        return ptrs, self.ranks[0], buf
+
+    def remote_done(self):
+        self._symm_hdl.barrier()       # every rank's stores have landed before anyone reads
+        self._symm = None              # the received shard is now this rank's state
 
 
 def _flat(t):
@@ -382,12 +420,18 @@ class EngineExecutor:
     def zeros(self, rows, dim):
         return self.torch.zeros((rows, dim), dtype=self.torch.complex64, device=self.device)
 
-    def apply(self, circuits, names, values, psi, observables=None):
-        """observables: None, or one local observable per row (rows differ in signs only)."""
+    def apply(self, circuits, names, values, psi, observables=None, remote=None):
+        """observables: None, or one local observable per row (rows differ in signs only).
+        remote: (peer pointers, rank of row 0, g) -- the last pass writes the swapped shards
+        (only when every row shares one structure and no padding is needed)."""
         from .engine import ENGINE
 
         torch = self.torch
         theta = torch.as_tensor(np.asarray(values, dtype=np.float32)).to(self.device).reshape(len(circuits), -1)
+        if remote is not None:
+            b = ENGINE.bind(circuits, names, [], from_state=True, want_state=True, device=self.device)
+            b.execute(theta, initial=psi, donate=True, want_state=False, want_expect=False, remote=remote)
+            return psi, None
         if observables is None:
             # ranks whose restricted circuits differ in structure (e.g. the sign of a
             # symbolic Z term on a global qubit) run as separate batches
@@ -420,8 +464,16 @@ class EngineExecutor:
         return psi, torch.stack(vals)
 
 
+def _can_fuse(circuits, names, n_loc):
+    if n_loc < pl.N_MIN:
+        return False
+    sym_index = {s: i for i, s in enumerate(names)}
+    key = pl.topology_key(circuits[0], sym_index)
+    return all(pl.topology_key(c, sym_index) == key for c in circuits[1:])
+
+
 def run_sharded(circuit, observable, g: int, exchange, executor=None, symbol_names=(), values=None,
-                plan: DistPlan | None = None, timer=None):
+                plan: DistPlan | None = None, timer=None, fuse_swaps: bool = True):
     """Expectation of ``observable`` after ``circuit`` on a state sharded over 2^g ranks.
 
     ``exchange``: LoopbackExchange(g) (all shards here) or NcclExchange(g) (this rank's shard).
@@ -441,6 +493,7 @@ def run_sharded(circuit, observable, g: int, exchange, executor=None, symbol_nam
             psi[i, 0] = 1.0
     last_seg = max(k for k, s in enumerate(plan.steps) if s.kind == "segment")
     result = None
+    skip_swap = False
     for k, (step, pos) in enumerate(zip(plan.steps, plan.pos_before)):
         if timer:
             timer(step.kind, k)
@@ -451,10 +504,26 @@ def run_sharded(circuit, observable, g: int, exchange, executor=None, symbol_nam
             if k == last_seg:
                 obs = [localize_observable(observable, pos, n_loc, r) for r in ranks]
                 psi, result = executor.apply(circs, names, vals, psi, obs)
+                continue
+            nxt = plan.steps[k + 1] if k + 1 < len(plan.steps) else None
+            targets = None
+            if (fuse_swaps and nxt is not None and nxt.kind == "swap" and step.gates and
+                    isinstance(executor, EngineExecutor) and hasattr(exchange, "remote_targets") and
+                    _can_fuse(circs, names, n_loc)):
+                targets = exchange.remote_targets(psi)
+            if targets is not None:
+                # the segment's last pass stores straight into the receive shards (fused swap)
+                ptrs, rank0, recv = targets
+                executor.apply(circs, names, vals, psi, None, remote=(ptrs.data_ptr(), rank0, g))
+                exchange.remote_done()
+                psi = recv
+                skip_swap = True
             else:
                 psi, _ = executor.apply(circs, names, vals, psi, None)
         elif step.kind == "permute":
             psi = permute_local_bits(psi, step.perm, n_loc)
+        elif skip_swap:
+            skip_swap = False
         else:
             psi = exchange.swap(psi, n_loc)
     if timer:

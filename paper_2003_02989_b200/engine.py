@@ -89,11 +89,11 @@ class DeviceProgram:
             term_const=_ptr(const_t), const_rows=const_rows, n_const=max(self.n_const, 1),
         )
 
-    def jit(self, device, rows: int):
+    def jit(self, device, rows: int, force: bool = False):
         """Plan-specialised kernels for this program (compiled on first use) or None."""
         from . import jit as _jit
 
-        if not _jit.enabled(rows, self.prog.n):
+        if not force and not _jit.enabled(rows, self.prog.n):
             return None
         if self._jit is None:
             with _JIT_LOCK:
@@ -279,7 +279,7 @@ class Bound:
         return len(self.circuits)
 
     def execute(self, theta: torch.Tensor, *, upstream=None, want_state=False, want_grad=False,
-                want_expect=True, stream=None, initial=None, donate=False) -> dict:
+                want_expect=True, stream=None, initial=None, donate=False, remote=None) -> dict:
         """theta: device float32 [B, S]; initial: [B, 2^n] complex state when bound
         ``from_state`` (the circuit is applied to it instead of |0...0>; ``donate``: the
         caller's contiguous complex64 device tensor is updated in place).  Returns device tensors."""
@@ -325,9 +325,10 @@ class Bound:
         else:
             frame_f = None
         partials = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
-        jf = fw.jit(dev, B)
+        jf = fw.jit(dev, B, force=remote is not None)
         if jf is not None:
-            jf.run(B, _ptr(psi), 0, _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), 0, _ptr(partials), stream)
+            jf.run(B, _ptr(psi), 0, _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), 0, _ptr(partials), stream,
+                   remote=remote)
         else:
             nat.check(lib.qf_run_passes(C.byref(fw.struct), 0, len(fw.prog.passes), _ptr(psi), n_eff, B,
                                         _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), _ptr(partials), fw.tiles,

@@ -40,7 +40,8 @@ def prelude() -> str:
 class QfJitArgs(C.Structure):
     _fields_ = [("psi", C.c_void_p), ("lam", C.c_void_p), ("mats", C.c_void_p), ("angles", C.c_void_p),
                 ("coefs", C.c_void_p), ("partials", C.c_void_p), ("n_mat", C.c_int), ("n_ang", C.c_int),
-                ("coef_stride", C.c_int), ("n_slots", C.c_int), ("tiles_log2", C.c_int), ("pad", C.c_int)]
+                ("coef_stride", C.c_int), ("n_slots", C.c_int), ("tiles_log2", C.c_int), ("pad", C.c_int),
+                ("peers", C.c_void_p), ("rank_base", C.c_int), ("pad2", C.c_int)]
 
 
 FUSED_GRAD = os.environ.get("QF_FUSED_GRAD", "0") not in ("0", "", "false")   # measured 2% slower
@@ -129,8 +130,12 @@ def _wht_code(vals: dict, R: int, kind: str, out: str, indent: str) -> list:
     return lines
 
 
-def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
-    """Per-pass CUDA kernel sources (without prelude), kernel names, launch geometry."""
+def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 0) -> tuple[list, list, list]:
+    """Per-pass CUDA kernel sources (without prelude), kernel names, launch geometry.
+
+    ``remote_pass``: that pass stores into the receive shards of the other ranks instead of
+    in place (a global-qubit swap fused into the pass, distributed.py): amplitude ``idx`` of
+    rank s goes to rank idx >> (n - g) at (idx & low) | (s << (n - g))."""
     n, L, R, adj = prog.n, prog.L, prog.R, prog.adjoint
     TB = L - R
     NR, NT = 1 << R, 1 << TB
@@ -145,7 +150,9 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
     src = []
     names, geo = [], []
     for pi, p in enumerate(prog.passes):
-        name = f"qf_{tag}_p{pi}"
+        if remote_pass >= 0 and pi != remote_pass:
+            continue
+        name = f"qf_{tag}_p{pi}" + ("_rs" if pi == remote_pass else "")
         names.append(name)
         sb, se = int(p[0]), int(p[1])
         init, store = int(p[2]), int(p[3])
@@ -613,10 +620,18 @@ def generate(prog: pl.Program, tag: str) -> tuple[list, list, list]:
         if store:
             stl = st_rows[-1]
             w(f"  {{ const u32 gs = base | {_xor_expr(tglob(stl))};")
-            w("    float2* __restrict__ pts = psi + gs;")
-            if adj:
+            if pi == remote_pass:
+                SH = n - remote_g
+                low = (1 << SH) - 1
+                w("    const u32 myr = (u32)(a.rank_base + row);")
+                for r in range(NR):
+                    w(f"    {{ const u32 idx = gs + {roff(stl, r)}u;"
+                      f" a.peers[idx >> {SH}][(size_t)((idx & {low}u) | (myr << {SH}))] = v0[{r}]; }}")
+            else:
+                w("    float2* __restrict__ pts = psi + gs;")
+            if adj and pi != remote_pass:
                 w("    float2* __restrict__ lts = lam + gs;")
-            for r in range(NR):
+            for r in (range(NR) if pi != remote_pass else []):
                 w(f"    pts[{roff(stl, r)}ll] = v0[{r}];")
                 if adj:
                     w(f"    lts[{roff(stl, r)}ll] = v1[{r}];")
@@ -725,6 +740,7 @@ class JitProgram:
         self.smem = (C.c_uint32 * P)(*[g[1] for g in geo])
         self.grid = (C.c_uint32 * P)()
         self.prog = prog
+        self._remote = {}
         self.persist = PERSIST
         sms = lib.qf_device_sm_count(device_index)
         self.resident = []
@@ -733,12 +749,44 @@ class JitProgram:
             nat.check(lib.qf_jit_occupancy(f, nt, smem, C.byref(occ)))
             self.resident.append(max(1, occ.value) * max(1, sms))
 
-    def run(self, rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first=0, last=None):
+    def remote_pass(self, g: int):
+        """(function, block, smem) of the last pass with the fused swap store (compiled once per g)."""
+        hit = self._remote.get(g)
+        if hit is None:
+            lib = nat.load()
+            tag = "a" if self.prog.adjoint else "f"
+            srcs, names, geo = generate(self.prog, tag, remote_pass=len(self.prog.passes) - 1, remote_g=g)
+            img = compile_kernel(srcs[0], names[0] + f"_g{g}")
+            mod = C.c_void_p()
+            nat.check(lib.qf_jit_load(img, C.byref(mod)))
+            f = C.c_void_p()
+            nat.check(lib.qf_jit_function(mod, names[0].encode(), max(geo[0][1], 48 * 1024), C.byref(f)))
+            self.modules.append(mod)
+            hit = self._remote[g] = (f.value, geo[0][0], geo[0][1])
+        return hit
+
+    def run(self, rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first=0, last=None,
+            remote=None):
+        """remote = (device array of the ranks' receive-shard pointers, rank of row 0, g): the
+        last pass writes its output into those shards (a fused global-qubit swap)."""
         lib = nat.load()
         last = self.n if last is None else last
         args = QfJitArgs(psi=psi, lam=lam, mats=mats, angles=angles, coefs=coefs, partials=partials,
                          n_mat=self.prog.n_mat, n_ang=self.prog.n_ang, coef_stride=coef_stride,
                          n_slots=self.prog.n_slots, tiles_log2=self.rows_shift, pad=rows)
+        if remote is not None:
+            peers, rank_base, g = remote
+            args.peers, args.rank_base = peers, rank_base
+            if last == self.n:
+                if last - 1 > first:
+                    self.run(rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first, last - 1)
+                f, nt, smem = self.remote_pass(g)
+                funcs = (C.c_void_p * 1)(f)
+                grid = (C.c_uint32 * 1)(rows << self.rows_shift)
+                block = (C.c_uint32 * 1)(nt)
+                sm = (C.c_uint32 * 1)(smem)
+                nat.check(lib.qf_jit_run(funcs, grid, block, sm, 1, stream, C.byref(args), C.sizeof(args)))
+                return
         total = rows << self.rows_shift
         for i in range(self.n):
             self.grid[i] = min(total, self.resident[i]) if self.persist else total

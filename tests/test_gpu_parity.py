@@ -505,3 +505,17 @@ def test_sampled_expectation_band_over_seeds(cuda):
     vals = np.array([sim.sampled_expectation(c, obs, 200, seed=s) for s in range(100)])
     sigma = np.sqrt(2.0 / 200 / 100)
     assert abs(vals.mean() - exact) < 5 * sigma
+
+
+def test_fused_swap_pass_matches_all_to_all(cuda):
+    """The global-qubit swap fused into the preceding pass (remote stores into the ranks'
+    receive shards) gives the same sharded result as the separate all-to-all."""
+    from paper_2003_02989_b200 import distributed as D
+
+    c = wl.brickwork_circuit(22, 10, wl.SEED_BIG)
+    obs = wl.z_sum(22)
+    for g in (1, 2, 3):
+        fused, plan = D.run_sharded(c, obs, g, D.LoopbackExchange(g), fuse_swaps=True)
+        plain, _ = D.run_sharded(c, obs, g, D.LoopbackExchange(g), fuse_swaps=False)
+        assert plan.swaps >= 1
+        assert fused == pytest.approx(plain, abs=1e-6)
