@@ -145,3 +145,29 @@ def test_gloo_sharded_state_matches_oracle(tmp_path, g):
     syms = circuit_symbols(c)
     assert swaps >= 1
     assert e == pytest.approx(_reference(c, obs, np.linspace(-0.7, 1.9, len(syms))), abs=1e-10)
+
+
+@pytest.mark.parametrize("n_loc,g", [(6, 1), (7, 2), (8, 3)])
+def test_fused_swap_addressing_equals_all_to_all(n_loc, g):
+    """The remote-store pass (jit.generate(remote_pass=...)) sends local amplitude idx of
+    rank s to rank idx >> (n-g) at (idx & low) | (s << (n-g)); that is exactly the
+    all-to-all the exchanges perform (LoopbackExchange.swap)."""
+    import torch
+
+    from paper_2003_02989_b200 import jit, planner as pl
+
+    R = 1 << g
+    psi = torch.arange(R << n_loc, dtype=torch.float64).reshape(R, -1).to(torch.complex128)
+    want = D.LoopbackExchange(g).swap(psi.clone(), n_loc)
+    got = torch.zeros_like(psi)
+    SH, low = n_loc - g, (1 << (n_loc - g)) - 1
+    for s in range(R):
+        for idx in range(1 << n_loc):
+            got[idx >> SH, (idx & low) | (s << SH)] = psi[s, idx]
+    assert torch.equal(got, want)
+    # and the generated kernel uses that formula
+    c = wl.brickwork_circuit(12, 2, 1)
+    prog = pl.build_program(c, pl.analyse(c, {}), 12, adjoint=False)
+    src, names, _ = jit.generate(prog, "f", remote_pass=len(prog.passes) - 1, remote_g=2)
+    assert names == [f"qf_f_p{len(prog.passes) - 1}_rs"]
+    assert "a.peers[idx >> 10][(size_t)((idx & 1023u) | (myr << 10))]" in src[0]
