@@ -393,7 +393,10 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         for si, st in enumerate(st_rows):
             if si:
                 prev = st_rows[si - 1]
-                w("  __syncthreads();")
+                if si > 1 or PERSIST:
+                    # readers of the previous exchange must be done before it is overwritten
+                    # (the first exchange of a tile has no earlier readers of this buffer)
+                    w("  __syncthreads();")
                 w(f"  {{ const u32 tp = {_xor_expr(tphys(prev))};")
                 for r in range(NR):
                     w(f"    sm[tp ^ {roff(prev, r, True)}u] = v0[{r}];")
@@ -647,7 +650,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 for i in range(32):
                     w(f"    x[{i}] = {f'GS[{(c0 + i) * NT} + t]' if i < K else '0.f'};")
                 w("    warp_transpose_sum32(x, t & 31u);")
-                w("    __syncthreads();")
+                if c0 or PERSIST:
+                    w("    __syncthreads();")   # the previous chunk's cross-warp reads are done
                 w(f"    WS[(t >> 5) * 32 + (t & 31)] = x[0];")
                 w("    __syncthreads();")
                 w(f"    if (t < {K}) {{ double acc = 0.0;")
