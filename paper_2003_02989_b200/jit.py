@@ -45,6 +45,7 @@ class QfJitArgs(C.Structure):
 
 
 FUSED_GRAD = os.environ.get("QF_FUSED_GRAD", "0") not in ("0", "", "false")   # measured 2% slower
+CHUNKED_GS = os.environ.get("QF_CHUNKED_GS", "1") not in ("0", "", "false")
 GS_THREAD_BYTES = int(os.environ.get("QF_GS_BYTES", str(40 * 1024)))
 # 0: one CTA per tile; 1: persistent CTAs (measured slower); 2: persistent CTAs that prefetch
 # the next tile into shared memory with cp.async while computing the current one
@@ -167,9 +168,12 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         # slot partials: one float per thread and slot, or (many slots) one per warp after a
         # shuffle reduction, so the CTA keeps its occupancy
         per_thread_gs = scnt * NT * 4 <= GS_THREAD_BYTES
-        GSW = NT if per_thread_gs else NT // 32
-        ws_floats = (NT // 32) * 32 if (scnt and per_thread_gs) else 0
-        smem = NA * TILE * 8 + mcnt * 16 + acnt * 4 + ccnt * 4 + scnt * GSW * 4 + ws_floats * 4 + 16
+        # many slots: a ring of 16 per-thread slots flushed by a 16-value warp transpose-reduction
+        chunked = (not per_thread_gs) and CHUNKED_GS and NT >= 64
+        GSW = NT if (per_thread_gs or chunked) else NT // 32
+        ws_floats = (NT // 32) * 32 if (scnt and (per_thread_gs or chunked)) else 0
+        gs_slots = min(scnt, 16) if chunked else scnt
+        smem = NA * TILE * 8 + mcnt * 16 + acnt * 4 + ccnt * 4 + gs_slots * GSW * 4 + ws_floats * 4 + 16
         # integer-weight phase polynomials (full-WHT path only) get a per-CTA phase table
         int_tables = {}
         tbl_bytes = 0
@@ -204,9 +208,33 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     for op_ in pass_ops)
         minb_p = min(minb, max(1, 65536 // (NT * 128))) if (heavy and not env_minb) else minb
 
+        flushes = [0]
+
+        def gs_flush(c0, K):
+            """Reduce ring slots [c0, c0+K) (ring position i = slot c0 + i) into partials."""
+            NWP = NT // 32
+            code = ["{ float x[16];"]
+            code += [f"x[{i}] = {f'GS[{i * NT} + t]' if i < K else '0.f'};" for i in range(16)]
+            code.append("warp_transpose_sum16(x, t & 31u);")
+            if flushes[0]:
+                code.append("__syncthreads();")
+            code.append("if ((t & 16u) == 0u) WS[(t >> 5) * 32 + (t & 15u)] = x[0];")
+            code.append("__syncthreads();")
+            code.append(f"if (t < {K}) {{ double acc = 0.0; for (int wv = 0; wv < {NWP}; ++wv) "
+                        f"acc += (double)WS[wv * 32 + t]; a.partials[((size_t)row * a.n_slots + {slb + c0} + t) * "
+                        f"{1 << (n - L)} + o] = acc; }}")
+            code.append("}")
+            flushes[0] += 1
+            return " ".join(code)
+
         def gs_store(slot_rel, expr):
             if per_thread_gs:
                 return f"GS[{slot_rel * NT} + t] = {expr};"
+            if chunked:
+                st = f"GS[{(slot_rel % 16) * NT} + t] = {expr};"
+                if slot_rel % 16 == 15:
+                    st += " " + gs_flush(slot_rel - 15, 16)
+                return st
             return f"{{ const float gsv = warp_sum_f({expr}); if ((t & 31u) == 0u) GS[{slot_rel * GSW} + (t >> 5)] = gsv; }}"
         geo.append((NT, smem))
         o = []
@@ -220,7 +248,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         w(f"  float* CO = reinterpret_cast<float*>(ANG + {acnt});")
         w(f"  float* GS = CO + {ccnt};")
         if ws_floats:
-            w(f"  float* WS = GS + {scnt * GSW};")
+            w(f"  float* WS = GS + {gs_slots * GSW};")
         if int_tables:
             w(f"  float4* TB = reinterpret_cast<float4*>(smem_raw + {(pf_off - tbl_bytes)});")
         if prefetch:
@@ -639,7 +667,10 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 if adj:
                     w(f"    lts[{roff(stl, r)}ll] = v1[{r}];")
             w("  }")
-        if scnt and per_thread_gs and NT >= 64:
+        if scnt and chunked:
+            if scnt % 16:
+                w("  " + gs_flush(scnt - scnt % 16, scnt % 16))
+        elif scnt and per_thread_gs and NT >= 64:
             # each thread's slot values are its own GS entries: per 32-slot chunk, a warp
             # transpose-reduction leaves slot L's warp sum on lane L; warps combine in order
             NWP = NT // 32

@@ -519,3 +519,26 @@ def test_fused_swap_pass_matches_all_to_all(cuda):
         plain, _ = D.run_sharded(c, obs, g, D.LoopbackExchange(g), fuse_swaps=False)
         assert plan.swaps >= 1
         assert fused == pytest.approx(plain, abs=1e-6)
+
+
+def test_qcnn16_plan_specialised_many_slot_passes(cuda, monkeypatch):
+    """Config-3 QCNN at 16 qubits through the plan-specialised kernels: passes with more
+    gradient slots than fit per thread use the 16-slot ring flushed by warp
+    transpose-reductions; gradients against the oracle's adjoint."""
+    from paper_2003_02989_b200.engine import ENGINE
+
+    monkeypatch.setenv("QF_JIT", "1")
+    ENGINE._bound.clear()
+    phis, _, params = wl.qcnn_data(2, 16)
+    model = wl.qcnn_model(16)
+    circs = [Circuit(16, list(wl.qcnn_data_circuit(p).gates) + list(model.gates)) for p in phis]
+    syms = circuit_symbols(model)
+    obs = PauliSum([PauliString(1.0, {15: "Z"})])
+    e, g = ops.expectation_and_gradient(circs, syms, params, [obs])
+    b = ENGINE.bind(circs, syms, [obs], want_grad=True)
+    assert max(int(p[9] - p[8]) for p in b.plan.adj.prog.passes) > 40     # ring mode exercised
+    for r in range(2):
+        bind = dict(zip(syms, params[r].astype(np.float64)))
+        ee, gg = orc.adjoint_grad(circs[r], obs, bind)
+        assert e[r, 0] == pytest.approx(ee, abs=EXP)
+        _close_grad(g[r], gg)
