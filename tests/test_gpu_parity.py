@@ -542,3 +542,59 @@ def test_qcnn16_plan_specialised_many_slot_passes(cuda, monkeypatch):
         ee, gg = orc.adjoint_grad(circs[r], obs, bind)
         assert e[r, 0] == pytest.approx(ee, abs=EXP)
         _close_grad(g[r], gg)
+
+
+# ---------------------------------------------------------------------------
+# layer entry points (ref graph.py:443-549) with a PQC-shaped node
+# ---------------------------------------------------------------------------
+
+
+class _Node:
+    """The attributes quantum_forward/backward use of the reference's _QuantumNode."""
+
+    def __init__(self, model, data, observables, differentiator, estimator=None):
+        self.name = "pqc"
+        self.model_circuit = model
+        self.symbols = circuit_symbols(model)
+        self.observables = observables
+        self.differentiator = differentiator
+        self.estimator = estimator if estimator is not None else gr.Exact()
+        self._data = data
+        self._calls = 0
+
+    def _data_batch(self, rows):
+        return self._data[:rows]
+
+    def _combined(self, d):
+        return Circuit(self.model_circuit.num_qubits, list(d.gates) + list(self.model_circuit.gates))
+
+    def _next_call(self):
+        self._calls += 1
+        return self._calls
+
+
+@pytest.mark.parametrize("diff", ["adjoint", "ps", "fd"])
+def test_layer_forward_backward_equal_materialised_jacobian(cuda, diff):
+    """quantum_backward is the vector-Jacobian product of quantum_forward (ref
+    test_graph.py:161-180): compared with the oracle's per-row, per-observable gradients."""
+    from paper_2003_02989_b200 import graph
+
+    rng = np.random.default_rng(91)
+    model = wl.qcnn_model(8)
+    data = [wl.qcnn_data_circuit(rng.uniform(-np.pi, np.pi, 8)) for _ in range(3)]
+    obs = [PauliSum([PauliString(1.0, {7: "Z"})]), random_observable(rng, 8, k=3)]
+    d = {"adjoint": gr.Adjoint(), "ps": gr.ParameterShift(), "fd": gr.FiniteDifference(epsilon=1e-3)}[diff]
+    node = _Node(model, data, obs, d)
+    pb = rng.uniform(0, 2, size=(3, len(node.symbols))).astype(np.float32).astype(np.float64)
+    up = rng.normal(size=(3, 2))
+    fwd = graph.quantum_forward(node, pb)
+    vjp = graph.quantum_backward(node, pb, up)
+    for b in range(3):
+        c = node._combined(data[b])
+        bind = dict(zip(node.symbols, pb[b]))
+        amps = orc.simulate_amps(c, bind)
+        for k, o in enumerate(obs):
+            assert fwd[b, k] == pytest.approx(orc.expectation(amps, o, 8), abs=EXP)
+        jac = np.stack([orc.adjoint_grad(c, o, bind)[1] for o in obs])      # [n_obs, S]
+        tol = 2e-3 if diff == "fd" else GABS
+        np.testing.assert_allclose(vjp[b], up[b] @ jac, atol=tol, rtol=GREL)
