@@ -598,3 +598,51 @@ def test_layer_forward_backward_equal_materialised_jacobian(cuda, diff):
         jac = np.stack([orc.adjoint_grad(c, o, bind)[1] for o in obs])      # [n_obs, S]
         tol = 2e-3 if diff == "fd" else GABS
         np.testing.assert_allclose(vjp[b], up[b] @ jac, atol=tol, rtol=GREL)
+
+
+def test_gpu_evaluator_protocol_and_stochastic_ps(cuda):
+    """The evaluator protocol (ref gradients.py:96-110) on the GPU: exact PS through a
+    GpuEvaluator equals the batched PS and counts its evaluations; stochastic PS over
+    coordinates / generator terms / cost terms is unbiased within 4 sigma over seeds (ref
+    test_gradients.py:275-325)."""
+    rng = np.random.default_rng(13)
+    c = Circuit(3, [G.ry(ParamExpr("a"), 0), G.cnot_pow(ParamExpr("b", 0.7), 0, 1), G.rx(ParamExpr("a", -0.5), 2),
+                    G.cz(1, 2), wl.pauli_pair_pow("X", "b", 1, 2)])
+    o = PauliSum([PauliString(0.8, {0: "Z"}), PauliString(-1.2, {1: "X", 2: "Z"}), PauliString(0.5, {2: "Y"})])
+    bind = {"a": 0.37, "b": -0.81}
+    req = gr.GradRequest(c, o, bind)
+    exact = gr.parameter_shift_grad(req)
+    ev = gr.GpuEvaluator()
+    viaev = gr.parameter_shift_grad(req, evaluator=ev)
+    np.testing.assert_allclose(viaev.gradient, exact.gradient, atol=1e-5)
+    assert ev.count == viaev.evaluations == exact.evaluations
+    cfg = dict(sample_generator_terms=True, sample_cost_terms=True, sample_coordinates=True)
+    draws = np.array([gr.stochastic_ps_grad(req, gr.StochasticConfig(**cfg, seed=s)).gradient for s in range(300)])
+    sem = draws.std(axis=0, ddof=1) / np.sqrt(len(draws))
+    assert np.all(np.abs(draws.mean(axis=0) - exact.gradient) < 4 * sem + 1e-6)
+    again = gr.stochastic_ps_grad(req, gr.StochasticConfig(**cfg, seed=5)).gradient
+    np.testing.assert_array_equal(again, draws[5])                         # seeded determinism
+
+
+def test_layer_forward_sampled_estimator(cuda):
+    """Sampled estimator in quantum_forward: per-row seeds derive_seed(seed, call_id, b, k)
+    (ref graph.py:463-467) -- reproducible for the same call id, within 5 sigma of exact."""
+    from paper_2003_02989_b200 import graph
+    from paper_2003_02989_b200.sampling import derive_seed
+
+    rng = np.random.default_rng(5)
+    model = wl.qcnn_model(4)
+    data = [wl.qcnn_data_circuit(rng.uniform(-np.pi, np.pi, 4)) for _ in range(4)]
+    obs = [PauliSum([PauliString(1.0, {3: "Z"})])]
+    pb = rng.uniform(0, 2, size=(4, len(circuit_symbols(model))))
+    exact = graph.quantum_forward(_Node(model, data, obs, gr.Adjoint()), pb)
+    n1 = _Node(model, data, obs, gr.Adjoint(), gr.Sampled(4000, seed=3))
+    n2 = _Node(model, data, obs, gr.Adjoint(), gr.Sampled(4000, seed=3))
+    s1, s2 = graph.quantum_forward(n1, pb), graph.quantum_forward(n2, pb)
+    np.testing.assert_array_equal(s1, s2)
+    assert np.all(np.abs(s1 - exact) < 5 * np.sqrt(1.0 / 4000))
+    # the seeds are the reference's: row b of call 1 draws with derive_seed(3, 1, b, 0)
+    c0 = n1._combined(data[0])
+    syms = circuit_symbols(model)
+    want = ops.sampled_expectation(c0, syms, pb[:1].astype(np.float32), obs, 4000, seed=[derive_seed(3, 1, 0, 0)])
+    assert s1[0, 0] == pytest.approx(float(want[0, 0]), abs=1e-12)
