@@ -770,7 +770,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         # dense two-qubit blocks hold 16 matrix pairs in registers: with 32 amplitudes per
         # thread they spill, so programs with many of them use 16 amplitudes per thread
         n2 = sum(o.kind == OP_DENSE2 for o in ops)
-        if n2 * 10 > len(ops):
+        if n2 * 2 > len(ops):
             L, R = 11, 4   # FP32-bound dense programs: smaller tiles, more CTAs (RCS 24q: 162 vs 167 ms)
     L = min(L, n)
     frame = frame and frame_eligible(ops, infos, adjoint)
