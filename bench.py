@@ -182,8 +182,10 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------
 
 
-def pass_bytes(prog, rows):
-    """Algorithmic HBM bytes of each pass launch (SURVEY 8(d) roofline rule)."""
+def pass_bytes(prog, rows, ckpt=False):
+    """Algorithmic HBM bytes of each pass launch (SURVEY 8(d) roofline rule).  ``ckpt``:
+    checkpointed adjoint -- backward passes read psi from a forward checkpoint and store
+    only lambda."""
     from paper_2003_02989_b200 import planner as pl
 
     amps = (1 << prog.n) * rows
@@ -192,7 +194,7 @@ def pass_bytes(prog, rows):
         init, store = int(p[2]), int(p[3])
         arrays = 2 if prog.adjoint else 1
         rd = 0 if init in (pl.INIT_ZERO, pl.INIT_PRODUCT) else (8 if init == pl.INIT_LOAD_PSI else 8 * arrays)
-        wr = 8 * arrays if store else 0
+        wr = (8 if ckpt else 8 * arrays) if (store and prog.adjoint) else (8 if store else 0)
         out.append((rd + wr) * amps)
     return out
 
@@ -267,23 +269,29 @@ def run_gpu(args, rank, world):
                                _ptr(angs_f), fw.prog.n_ang, s))
     nat.check(lib.qf_build_ops(C.byref(rec_a), _ptr(theta), theta.shape[1], B, _ptr(mats_a), ad.prog.n_mat,
                                _ptr(angs_a), ad.prog.n_ang, s))
+    ckpt = bound._checkpoints(psi, True)   # the same checkpoint buffers execute() uses
     if fw.frame:  # the same per-row Pauli-frame rewrite execute() performs
         sc_f = torch.empty((B, max(fw.prog.n_slots, 1)), dtype=torch.float64, device=dev)
         sc_a = torch.empty((B, max(ad.prog.n_slots, 1)), dtype=torch.float64, device=dev)
         fr = torch.empty((B, 2), dtype=torch.float64, device=dev)
-        nat.check(lib.qf_frame_walk(_ptr(fw.t_events), fw.n_events, 0, B, _ptr(mats_f), fw.prog.n_mat, _ptr(angs_f),
-                                    fw.prog.n_ang, _ptr(sc_f), fw.prog.n_slots, None, _ptr(fr), s))
-        nat.check(lib.qf_frame_walk(_ptr(ad.t_events), ad.n_events, 1, B, _ptr(mats_a), ad.prog.n_mat, _ptr(angs_a),
-                                    ad.prog.n_ang, _ptr(sc_a), ad.prog.n_slots, _ptr(fr), None, s))
+        pm = (_ptr(ckpt[1]), ckpt[1].shape[1]) if ckpt else (None, 0)
+        nat.check(lib.qf_frame_walk_ckpt(_ptr(fw.t_events), fw.n_events, 0, B, _ptr(mats_f), fw.prog.n_mat,
+                                         _ptr(angs_f), fw.prog.n_ang, _ptr(sc_f), fw.prog.n_slots, None, _ptr(fr),
+                                         pm[0], pm[1], s))
+        nat.check(lib.qf_frame_walk_ckpt(_ptr(ad.t_events), ad.n_events, 1, B, _ptr(mats_a), ad.prog.n_mat,
+                                         _ptr(angs_a), ad.prog.n_ang, _ptr(sc_a), ad.prog.n_slots, _ptr(fr), None,
+                                         pm[0], pm[1], s))
     part_f = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
     part_a = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
     hw = torch.ones((B, max(len(bound.hkeys), 1)), dtype=torch.float32, device=dev)
     struct_a = nat.QfProgram.from_buffer_copy(ad.struct)
     struct_a.coef_row_stride = hw.shape[1]
-    fb, ab = pass_bytes(fw.prog, B), pass_bytes(ad.prog, B)
+    fb, ab = pass_bytes(fw.prog, B), pass_bytes(ad.prog, B, ckpt=ckpt is not None)
+    ck = [_ptr(t) for t in ckpt[0]] if ckpt else None
     jf, ja = fw.jit(dev, B), ad.jit(dev, B)
     kname = (f"plan-specialised NVRTC tile-pass kernels qf_f_p*/qf_a_p* (forward L{fw.prog.L}/R{fw.prog.R}, "
-             f"adjoint L{ad.prog.L}/R{ad.prog.R}, Pauli-frame normalised={bool(fw.frame)})"
+             f"adjoint L{ad.prog.L}/R{ad.prog.R}, Pauli-frame normalised={bool(fw.frame)}, "
+             f"checkpointed adjoint={ckpt is not None})"
              if jf is not None else "qf::pass_kernel (interpreted)")
     reps = 5
     samp_f, samp_a = [], []
@@ -291,7 +299,10 @@ def run_gpu(args, rank, world):
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(fb) + len(ab) + 1)]
         ev[0].record(stream)
         for p in range(len(fb)):
-            if jf is not None:
+            if ck:
+                jf.run_ckpt(B, ck, [0] + ck[:-1], 0, _ptr(mats_f), _ptr(angs_f), _ptr(bound.fwd_coefs), 0,
+                            _ptr(part_f), s, False, which=[p])
+            elif jf is not None:
                 jf.run(B, _ptr(psi), 0, _ptr(mats_f), _ptr(angs_f), _ptr(bound.fwd_coefs), 0, _ptr(part_f), s,
                        first=p, last=p + 1)
             else:
@@ -299,7 +310,10 @@ def run_gpu(args, rank, world):
                                             _ptr(angs_f), _ptr(bound.fwd_coefs), _ptr(part_f), fw.tiles, s))
             ev[1 + p].record(stream)
         for p in range(len(ab)):
-            if ja is not None:
+            if ck:
+                ja.run_ckpt(B, ck[::-1], None, _ptr(lam), _ptr(mats_a), _ptr(angs_a), _ptr(hw), hw.shape[1],
+                            _ptr(part_a), s, True, which=[p])
+            elif ja is not None:
                 ja.run(B, _ptr(psi), _ptr(lam), _ptr(mats_a), _ptr(angs_a), _ptr(hw), hw.shape[1], _ptr(part_a), s,
                        first=p, last=p + 1)
             else:

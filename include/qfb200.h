@@ -183,6 +183,13 @@ int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, fl
                   int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
                   QfFrame* frame_out, void* stream);
 
+/* qf_frame_walk for checkpointed adjoint sweeps: pass-boundary events record the stored
+ * state's scale per forward pass into pass_m [rows, n_pass] (forward) or reload it from there
+ * (adjoint, whose passes read psi from the forward's pass outputs). */
+int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int rows, float* mats, int n_mat,
+                       int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
+                       QfFrame* frame_out, double* pass_m, int n_pass, void* stream);
+
 /* Generic Pauli-sum expectation partials: partials[row, k, chunk] = coef[row, k] *
  * sum_{x in chunk} Re(conj(psi[x ^ xm_k]) i^{ny_k} (-1)^{popc(x & zm_k)} psi[x]);
  * chunks = ceil(2^n / 2048).  Sum with qf_reduce_slots (slots = terms, tiles = chunks).

@@ -414,7 +414,7 @@ __device__ void frame_pauli(int a, int b, Z (&P)[4]) {  // X^a Z^b, row-major 2x
 
 __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adjoint, int row, float2* M,
                                int32_t* angles, int n_ang, double* slot_scale, int n_slots,
-                               const QfFrame* frame_in, QfFrame* frame_out) {
+                               const QfFrame* frame_in, QfFrame* frame_out, double* pass_m, int n_pass) {
   uint32_t x = 0, z = 0;
   double m = 1.0;
   if (frame_in) {
@@ -422,6 +422,10 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
     z = frame_in[row].z;
     m = frame_in[row].m;
   }
+  // mp: scale of the stored psi.  It equals m unless the adjoint sweep reloads psi from the
+  // forward's pass checkpoints (EV_PASS), whose scale the forward walk recorded; slot sums
+  // of <lambda|G|psi> then scale by sqrt(m * mp).
+  double mp = m;
   for (int e = 0; e < n_ev; ++e) {
     const int32_t* E = ev + (size_t)e * 8;
     const int kind = E[0], q0 = E[1], q1 = E[2], off = E[3], slot = E[4], col = E[5];
@@ -429,7 +433,10 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
       const uint32_t bit = 1u << q0;
       const int ax = (x & bit) ? 1 : 0, bz = (z & bit) ? 1 : 0;
       const int flip = kind == 1 ? bz : (ax ^ bz);
-      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = flip ? -m : m;
+      if (slot >= 0) {
+        const double sc = mp == m ? m : sqrt(m * mp);
+        slot_scale[(size_t)row * n_slots + slot] = flip ? -sc : sc;
+      }
       Z u00 = {M[off].x, M[off].y}, u01 = {M[off + 1].x, M[off + 1].y}, u10 = {M[off + 2].x, M[off + 2].y};
       if (adjoint) {  // kernels of the adjoint sweep apply U^dag
         const Z t01 = u01;
@@ -445,11 +452,13 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
         tau = (sv.x * u00.x + sv.y * u00.y) / c2;
         if (flip) tau = -tau;
         m *= c2;
+        mp *= c2;
       } else {         // tau = -c/s
         double k = (u00.x * sv.x + u00.y * sv.y) / s2;
         if (flip) k = -k;
         tau = -k;
         m *= s2;
+        mp *= s2;
         x ^= bit;
         if (kind == 2) z ^= bit;
       }
@@ -464,7 +473,10 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
       flip ^= ((l0 == 2 || l0 == 3) && (x & b0)) ? 1 : 0;
       flip ^= ((l1 == 1 || l1 == 2) && (z & b1)) ? 1 : 0;
       flip ^= ((l1 == 2 || l1 == 3) && (x & b1)) ? 1 : 0;
-      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = flip ? -m : m;
+      if (slot >= 0) {
+        const double sc = mp == m ? m : sqrt(m * mp);
+        slot_scale[(size_t)row * n_slots + slot] = flip ? -sc : sc;
+      }
       // U = e^{i phi}(c I - i s P):  U[0][0] = e^{i phi} c,  U[xm][0] = -i s c0 e^{i phi} with
       // P|00> = c0 |xm>  (c0 = i per Y factor);  the adjoint uses U^dag: (U^dag)[xm][0] = conj(U[0][xm])
       const int xm = ((l0 == 1 || l0 == 2) ? 2 : 0) | ((l1 == 1 || l1 == 2) ? 1 : 0);
@@ -485,11 +497,13 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
         tau = (sv.x * u00.x + sv.y * u00.y) / c2;
         if (flip) tau = -tau;
         m *= c2;
+        mp *= c2;
       } else {
         double k = (u00.x * sv.x + u00.y * sv.y) / s2;
         if (flip) k = -k;
         tau = -k;
         m *= s2;
+        mp *= s2;
         if (l0 == 1 || l0 == 2) x ^= b0;
         if (l0 == 2 || l0 == 3) z ^= b0;
         if (l1 == 1 || l1 == 2) x ^= b1;
@@ -527,21 +541,28 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
           N[i * D + j] = acc;
         }
       for (int i = 0; i < D * D; ++i) M[off + i] = make_float2((float)N[i].x, (float)N[i].y);
-      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = m;  // gradient taken after the apply
+      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = mp == m ? m : sqrt(m * mp);  // after the apply
+    } else if (kind == 8) {  // pass boundary (checkpointed adjoint): record / reload psi's scale
+      if (pass_m) {
+        if (!adjoint) pass_m[(size_t)row * n_pass + E[6]] = m;
+        else mp = pass_m[(size_t)row * n_pass + E[6]];
+      }
     } else if (kind == 5 || kind == 6) {
       angles[(size_t)row * n_ang + col] = (int32_t)x;
-      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = m;
+      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = mp == m ? m : sqrt(m * mp);
     }
   }
   if (frame_out) frame_out[row] = QfFrame{x, z, m};
 }
+
 
 // One CTA per row: the row's matrix slab and the event list are staged in shared memory,
 // one thread walks the events (shared-memory latency instead of a global round trip per
 // event), the CTA writes the slab back.
 __global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int adjoint, int rows,
                                   float2* mats, int n_mat, int32_t* angles, int n_ang, double* slot_scale,
-                                  int n_slots, const QfFrame* frame_in, QfFrame* frame_out) {
+                                  int n_slots, const QfFrame* frame_in, QfFrame* frame_out, double* pass_m,
+                                  int n_pass) {
   extern __shared__ __align__(16) unsigned char fw_smem[];
   float2* Ms = reinterpret_cast<float2*>(fw_smem);
   int32_t* Es = reinterpret_cast<int32_t*>(Ms + n_mat);
@@ -551,7 +572,8 @@ __global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int 
   for (int i = threadIdx.x; i < n_ev * 8; i += blockDim.x) Es[i] = ev[i];
   __syncthreads();
   if (threadIdx.x == 0)
-    frame_walk_row(Es, n_ev, adjoint, row, Ms, angles, n_ang, slot_scale, n_slots, frame_in, frame_out);
+    frame_walk_row(Es, n_ev, adjoint, row, Ms, angles, n_ang, slot_scale, n_slots, frame_in, frame_out, pass_m,
+                   n_pass);
   __syncthreads();
   for (int i = threadIdx.x; i < n_mat; i += blockDim.x) M[i] = Ms[i];
 }
@@ -560,11 +582,11 @@ __global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int 
 __global__ void frame_walk_global_kernel(const int32_t* __restrict__ ev, int n_ev, int adjoint, int rows,
                                          float2* mats, int n_mat, int32_t* angles, int n_ang,
                                          double* slot_scale, int n_slots, const QfFrame* frame_in,
-                                         QfFrame* frame_out) {
+                                         QfFrame* frame_out, double* pass_m, int n_pass) {
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= rows) return;
   frame_walk_row(ev, n_ev, adjoint, row, mats + (size_t)row * n_mat, angles, n_ang, slot_scale, n_slots,
-                 frame_in, frame_out);
+                 frame_in, frame_out, pass_m, n_pass);
 }
 
 }  // namespace qf
@@ -678,9 +700,9 @@ int qf_reduce_slots_scaled(const double* partials, int rows, int n_slots, int ti
   return check_launch("reduce_slots_kernel");
 }
 
-int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, float* mats, int n_mat,
-                  int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
-                  QfFrame* frame_out, void* stream) {
+int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int rows, float* mats, int n_mat,
+                       int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
+                       QfFrame* frame_out, double* pass_m, int n_pass, void* stream) {
   if (rows == 0) return 0;
   const size_t smem = (size_t)n_mat * sizeof(float2) + (size_t)n_events * 8 * sizeof(int32_t);
   if (smem <= 96 * 1024) {
@@ -691,14 +713,21 @@ int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, fl
     }
     frame_walk_kernel<<<rows, 128, smem, (cudaStream_t)stream>>>(
         events, n_events, adjoint, rows, reinterpret_cast<float2*>(mats), n_mat, angles, n_ang, slot_scale,
-        n_slots, frame_in, frame_out);
+        n_slots, frame_in, frame_out, pass_m, n_pass);
     return check_launch("frame_walk_kernel");
   }
   const int T = 128;
   frame_walk_global_kernel<<<(rows + T - 1) / T, T, 0, (cudaStream_t)stream>>>(
       events, n_events, adjoint, rows, reinterpret_cast<float2*>(mats), n_mat, angles, n_ang, slot_scale, n_slots,
-      frame_in, frame_out);
+      frame_in, frame_out, pass_m, n_pass);
   return check_launch("frame_walk_global_kernel");
+}
+
+int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, float* mats, int n_mat,
+                  int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
+                  QfFrame* frame_out, void* stream) {
+  return qf_frame_walk_ckpt(events, n_events, adjoint, rows, mats, n_mat, angles, n_ang, slot_scale, n_slots,
+                            frame_in, frame_out, nullptr, 0, stream);
 }
 
 int qf_pauli_expect(const float* psi, int n, int rows, int n_terms, const uint32_t* xmask, const uint32_t* zmask,

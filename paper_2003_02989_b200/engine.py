@@ -314,19 +314,26 @@ class Bound:
         nat.check(lib.qf_build_ops(C.byref(rec), _ptr(theta), theta.shape[1], B, _ptr(mats), fw.prog.n_mat,
                                    _ptr(angs), fw.prog.n_ang, stream))
         scale = None
+        ckpt = self._checkpoints(psi, want_grad and not want_state and remote is None)
         if fw.frame:
             if want_state:
                 raise ValueError("this binding stores frame-normalised states (expectations / gradients "
                                  "only); bind with want_state=True for states")
             scale = torch.empty((B, max(fw.prog.n_slots, 1)), dtype=torch.float64, device=dev)
             frame_f = torch.empty((B, 2), dtype=torch.float64, device=dev)  # QfFrame {u32 x, z; f64 m}
-            nat.check(lib.qf_frame_walk(_ptr(fw.t_events), fw.n_events, 0, B, _ptr(mats), fw.prog.n_mat, _ptr(angs),
-                                        fw.prog.n_ang, _ptr(scale), fw.prog.n_slots, None, _ptr(frame_f), stream))
+            pm = (_ptr(ckpt[1]), ckpt[1].shape[1]) if ckpt else (None, 0)
+            nat.check(lib.qf_frame_walk_ckpt(_ptr(fw.t_events), fw.n_events, 0, B, _ptr(mats), fw.prog.n_mat,
+                                             _ptr(angs), fw.prog.n_ang, _ptr(scale), fw.prog.n_slots, None,
+                                             _ptr(frame_f), pm[0], pm[1], stream))
         else:
             frame_f = None
         partials = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
         jf = fw.jit(dev, B, force=remote is not None)
-        if jf is not None:
+        if ckpt:
+            ck = ckpt[0]
+            jf.run_ckpt(B, [_ptr(t) for t in ck], [0] + [_ptr(t) for t in ck[:-1]], 0, _ptr(mats), _ptr(angs),
+                        _ptr(self.fwd_coefs), 0, _ptr(partials), stream, False)
+        elif jf is not None:
             jf.run(B, _ptr(psi), 0, _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), 0, _ptr(partials), stream,
                    remote=remote)
         else:
@@ -355,10 +362,28 @@ class Bound:
             st = psi[:, : (1 << plan.n)]
             out["state"] = st.clone() if want_grad else st
         if want_grad:
-            self._adjoint(lib, psi, theta, upstream, stream, out, frame_f)
+            self._adjoint(lib, psi, theta, upstream, stream, out, frame_f, ckpt)
         return out
 
-    def _adjoint(self, lib, psi, theta, upstream, stream, out, frame_f=None):
+    def _checkpoints(self, psi, wanted):
+        """Checkpointed adjoint (plan.extra["ckpt"]): the forward passes write every pass
+        output to its own buffer, so the adjoint sweep reloads psi from them instead of
+        un-applying and storing it -- one state write per backward pass fewer, and exact
+        forward states.  Returns (buffers, pass scales [B, P]) or None when off / no room."""
+        plan = self.plan
+        if not (wanted and plan.extra.get("ckpt")):
+            return None
+        fw = plan.fwd
+        P = len(fw.prog.passes)
+        if fw.jit(self.device, self.B) is None or plan.adj.jit(self.device, self.B) is None:
+            return None
+        need = (P - 1) * psi.numel() * psi.element_size()
+        if need > 0.4 * torch.cuda.mem_get_info(self.device)[0]:
+            return None
+        ck = [torch.empty_like(psi) for _ in range(P - 1)] + [psi]
+        return ck, torch.empty((self.B, P), dtype=torch.float64, device=self.device)
+
+    def _adjoint(self, lib, psi, theta, upstream, stream, out, frame_f=None, ckpt=None):
         plan, dev, B = self.plan, self.device, self.B
         ad = plan.adj
         n_eff = plan.n_eff
@@ -379,9 +404,10 @@ class Bound:
         scale = None
         if ad.frame:
             scale = torch.empty((B, max(ad.prog.n_slots, 1)), dtype=torch.float64, device=dev)
-            nat.check(lib.qf_frame_walk(_ptr(ad.t_events), ad.n_events, 1, B, _ptr(mats), ad.prog.n_mat, _ptr(angs),
-                                        ad.prog.n_ang, _ptr(scale), ad.prog.n_slots, _ptr(frame_f), None,
-                                        stream))
+            pm = (_ptr(ckpt[1]), ckpt[1].shape[1]) if ckpt else (None, 0)
+            nat.check(lib.qf_frame_walk_ckpt(_ptr(ad.t_events), ad.n_events, 1, B, _ptr(mats), ad.prog.n_mat,
+                                             _ptr(angs), ad.prog.n_ang, _ptr(scale), ad.prog.n_slots, _ptr(frame_f),
+                                             None, pm[0], pm[1], stream))
         lam = torch.empty_like(psi)
         if not self.lam_diag:
             if self.hkeys:
@@ -392,7 +418,11 @@ class Bound:
                 lam.zero_()
         partials = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
         ja = ad.jit(dev, B)
-        if ja is not None:
+        if ckpt:
+            ck = ckpt[0]
+            ja.run_ckpt(B, [_ptr(t) for t in reversed(ck)], None, _ptr(lam), _ptr(mats), _ptr(angs), _ptr(hw_t),
+                        hw_t.shape[1], _ptr(partials), stream, True)
+        elif ja is not None:
             ja.run(B, _ptr(psi), _ptr(lam), _ptr(mats), _ptr(angs), _ptr(hw_t), hw_t.shape[1], _ptr(partials),
                    stream)
         else:
@@ -440,15 +470,34 @@ class Engine:
         diag_sums = [None] * len(obs.sums)
         for k in obs.diag_ids:
             diag_sums[k] = _TermList(obs.sums[k])
-        fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
-                               obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame)
-        plan = Plan(n, n_eff, len(symbol_index), infos, DeviceProgram(fwd, device), None, lam_diag, obs)
-        plan.extra["from_state"] = from_state
+        adjp = None
         if adjoint:
             infos_a = pl.analyse(template, symbol_index, overrides)
             hterms = _TermList([_Term(dict(kk), 1.0) for kk in hkeys])
             adjp = pl.build_program(template, infos_a, n_eff, adjoint=True, observables=[hterms],
                                     lam_diag=lam_diag, frame=frame)
+        ckpt = False
+        if adjp is not None and frame and lam_diag and not from_state and \
+                os.environ.get("QF_CKPT", "1") not in ("0", "", "false"):
+            fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
+                                   obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame, mirror=True)
+            # the adjoint's backward pass i must undo exactly forward pass P-1-i (both lists
+            # are in forward order), and both frame walks must hold the same Pauli frame at every
+            # pass boundary: true for normalised rotations and diagonal ops, not for general
+            # dense ops (the forward absorbs the frame in front of them, the adjoint behind)
+            ev = adjp.frame_events if adjp.frame_events is not None else np.zeros((0, pl.EV_INTS), np.int32)
+            ckpt = (fwd.frame and adjp.frame and fwd.stats["tile_qubits"] == adjp.stats["tile_qubits"]
+                    and fwd.stats["ops_per_pass"] == adjp.stats["ops_per_pass"]
+                    and not np.isin(np.asarray(ev)[:, 0], (pl.EV_ABS1, pl.EV_ABS2)).any())
+            if not ckpt:
+                infos = pl.analyse(template, symbol_index, overrides)
+        if not ckpt:
+            fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
+                                   obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame)
+        plan = Plan(n, n_eff, len(symbol_index), infos, DeviceProgram(fwd, device), None, lam_diag, obs)
+        plan.extra["from_state"] = from_state
+        plan.extra["ckpt"] = ckpt
+        if adjp is not None:
             assert adjp.frame == fwd.frame
             plan.adj = DeviceProgram(adjp, device)
             plan.extra["adj_infos"] = infos_a

@@ -41,7 +41,8 @@ class QfJitArgs(C.Structure):
     _fields_ = [("psi", C.c_void_p), ("lam", C.c_void_p), ("mats", C.c_void_p), ("angles", C.c_void_p),
                 ("coefs", C.c_void_p), ("partials", C.c_void_p), ("n_mat", C.c_int), ("n_ang", C.c_int),
                 ("coef_stride", C.c_int), ("n_slots", C.c_int), ("tiles_log2", C.c_int), ("pad", C.c_int),
-                ("peers", C.c_void_p), ("rank_base", C.c_int), ("pad2", C.c_int)]
+                ("peers", C.c_void_p), ("rank_base", C.c_int), ("pad2", C.c_int),
+                ("psi_src", C.c_void_p), ("skip_psi", C.c_int), ("pad3", C.c_int)]
 
 
 FUSED_GRAD = os.environ.get("QF_FUSED_GRAD", "0") not in ("0", "", "false")   # measured 2% slower
@@ -375,7 +376,10 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         elif init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI):
             # pointer + 64-bit constant offsets: u32 index sums above 2^29 elements were
             # miscompiled (half-width loads) by nvcc/NVRTC 12.9 at n >= 30
-            w("  const float2* __restrict__ pt0 = psi + gt0;")
+            if adj:
+                w("  const float2* __restrict__ pt0 = psi + gt0;")
+            else:
+                w(f"  const float2* __restrict__ pt0 = (a.psi_src ? a.psi_src + ((size_t)row << {n}) : psi) + gt0;")
             if adj and init == pl.INIT_LOAD:
                 w("  const float2* __restrict__ lt0 = lam + gt0;")
             for r in range(NR):
@@ -662,10 +666,15 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 w("    float2* __restrict__ pts = psi + gs;")
             if adj and pi != remote_pass:
                 w("    float2* __restrict__ lts = lam + gs;")
-            for r in (range(NR) if pi != remote_pass else []):
-                w(f"    pts[{roff(stl, r)}ll] = v0[{r}];")
-                if adj:
+            if adj and pi != remote_pass:
+                w("    if (!a.skip_psi) {")
+                for r in range(NR):
+                    w(f"      pts[{roff(stl, r)}ll] = v0[{r}];")
+                w("    }")
+                for r in range(NR):
                     w(f"    lts[{roff(stl, r)}ll] = v1[{r}];")
+            for r in (range(NR) if (pi != remote_pass and not adj) else []):
+                w(f"    pts[{roff(stl, r)}ll] = v0[{r}];")
             w("  }")
         if scnt and chunked:
             if scnt % 16:
@@ -799,6 +808,23 @@ class JitProgram:
             self.modules.append(mod)
             hit = self._remote[g] = (f.value, geo[0][0], geo[0][1])
         return hit
+
+    def run_ckpt(self, rows, psis, srcs, lam, mats, angles, coefs, coef_stride, partials, stream, skip_psi,
+                 which=None):
+        """One launch per pass with its own state pointers: psis[i] is pass i's state buffer,
+        srcs[i] (forward) the buffer it loads from (0 = psis[i]); skip_psi: adjoint passes
+        read psi from forward checkpoints and do not write it back."""
+        lib = nat.load()
+        for i in (range(self.n) if which is None else which):
+            args = QfJitArgs(psi=psis[i], lam=lam, mats=mats, angles=angles, coefs=coefs, partials=partials,
+                             n_mat=self.prog.n_mat, n_ang=self.prog.n_ang, coef_stride=coef_stride,
+                             n_slots=self.prog.n_slots, tiles_log2=self.rows_shift, pad=rows,
+                             psi_src=srcs[i] if srcs else 0, skip_psi=int(bool(skip_psi)))
+            total = rows << self.rows_shift
+            self.grid[i] = min(total, self.resident[i]) if self.persist else total
+            nat.check(lib.qf_jit_run(C.addressof(self.funcs) + C.sizeof(C.c_void_p) * i,
+                                     C.addressof(self.grid) + 4 * i, C.addressof(self.block) + 4 * i,
+                                     C.addressof(self.smem) + 4 * i, 1, stream, C.byref(args), C.sizeof(args)))
 
     def run(self, rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first=0, last=None,
             remote=None):

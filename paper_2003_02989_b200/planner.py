@@ -53,6 +53,7 @@ CLS_GENERAL, CLS_XLIKE, CLS_REAL = 0, 1, 2   # dense 1q matrix structure classes
 CLS_NX, CLS_NY = 3, 4                       # Pauli-frame normalised X / Y rotations: [[1, -i tau], [-i tau, 1]] / [[1, -tau], [tau, 1]]
 CLS_NP = 5                                  # normalised two-qubit Pauli-string rotation I - i tau P0 P1
 EV_NX, EV_NY, EV_ABS1, EV_ABS2, EV_DIAG, EV_OBS, EV_NP = 1, 2, 3, 4, 5, 6, 7   # frame-walk events
+EV_PASS = 8    # pass boundary: forward records the stored state's scale, adjoint reloads it
 PAULI_CODE = {"X": 1, "Y": 2, "Z": 3}
 EV_INTS = 8
 GK_MATRIX, GK_X, GK_Y, GK_Z = 0, 1, 2, 3     # adjoint generator kinds (GK_P: two-qubit Pauli string)
@@ -752,7 +753,7 @@ def frame_eligible(ops: list[Op], infos, adjoint: bool) -> bool:
 
 def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool,
                   observables=None, obs_diag_ids=(), lam_diag: bool = False,
-                  from_state: bool = False, frame: bool = False) -> Program:
+                  from_state: bool = False, frame: bool = False, mirror: bool = False) -> Program:
     """Plan + emit.  ``observables``: list of PauliSums; ``obs_diag_ids``: those fused as
     OBS ops at the end of the forward program; ``lam_diag``: adjoint with a diagonal H
     whose lambda-init / energy is fused into the first backward pass; ``from_state``:
@@ -764,9 +765,14 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     and the per-row frame (x, z, m) is tracked by the build step in execution order:
     general dense ops absorb the frame into their matrix, diagonal ops / observables are
     evaluated at index ^ x, and slot sums are scaled by m (and the generator's sign)."""
-    ops = build_ops(infos, adjoint)
+    # mirror: a forward program with exactly the adjoint program's ops and tile passes (no
+    # symbolic fusion, adjoint tile size), so its pass outputs are checkpoints the adjoint
+    # sweep can read and both Pauli-frame walks agree at every pass boundary
+    ops = build_ops(infos, adjoint or mirror)
     L, R = geometry(adjoint)
-    if not adjoint and R == 5 and "QF_GEOM_FWD" not in __import__("os").environ:
+    if mirror:
+        L = geometry(True)[0]
+    elif not adjoint and R == 5 and "QF_GEOM_FWD" not in __import__("os").environ:
         # dense two-qubit blocks hold 16 matrix pairs in registers: with 32 amplitudes per
         # thread they spill, so programs with many of them use 16 amplitudes per thread
         n2 = sum(o.kind == OP_DENSE2 for o in ops)
@@ -777,7 +783,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     if from_state and not adjoint:
         init = {}
     else:
-        ops, init = absorb_product_init(ops, infos, n, allow_symbolic=not adjoint)
+        ops, init = absorb_product_init(ops, infos, n, allow_symbolic=not (adjoint or mirror))
     # observable ops
     obs_ops = []
     if not adjoint:
@@ -838,6 +844,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         if not adjoint and first_fwd:
             for q, op in sorted(init.items()):
                 prow[48 + q] = em.dense_mat(op, (q,))
+        fwd_index = passes.index(p)
+        if frame and adjoint:
+            events.append([EV_PASS, -1, -1, -1, -1, -1, fwd_index, 0])
         for si, st in enumerate(stages):
             regs, thr = stage_slots(p, st, R)
             srow = np.zeros(STAGE_INTS, dtype=np.int32)
@@ -941,6 +950,8 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                 em.op_rows.append(orow)
             srow[49] = len(em.op_rows)
             em.stage_rows.append(srow)
+        if frame and not adjoint:
+            events.append([EV_PASS, -1, -1, -1, -1, -1, fwd_index, 0])
         prow[1] = len(em.stage_rows)
         prow[5] = em.n_mat
         prow[7] = em.n_ang

@@ -92,3 +92,27 @@ def rotation_circuit(rng, n, depth, n_sym):
                 gs.append(P1[rng.integers(6)](ParamExpr(names[rng.integers(n_sym)], float(rng.uniform(-1.5, 1.5)),
                                                         float(rng.uniform(-.5, .5))), q))
     return Circuit(n, gs)
+
+
+def pauli_rotation_circuit(rng, n, depth, n_sym):
+    """Symbolic rotations, constant Z-type rotations, Z and CZ only: every op is a normalised
+    rotation or diagonal under the Pauli frame (no dense op absorbs it), so the checkpointed
+    adjoint applies."""
+    names = [f"s{i}" for i in range(n_sym)]
+    gs = []
+    for _ in range(depth):
+        r = rng.random()
+        if n >= 2 and r < 0.25:
+            a, b = (int(q) for q in rng.choice(n, 2, replace=False))
+            gs.append(G.cz(a, b))
+        else:
+            q = int(rng.integers(n))
+            k = rng.random()
+            if k < 0.05:
+                gs.append(G.z(q))
+            elif k < 0.2:
+                gs.append((G.rz, G.zpow)[rng.integers(2)](float(rng.uniform(-3, 3)), q))
+            else:
+                gs.append(P1[rng.integers(6)](ParamExpr(names[rng.integers(n_sym)], float(rng.uniform(-1.5, 1.5)),
+                                                        float(rng.uniform(-.5, .5))), q))
+    return Circuit(n, gs)

@@ -374,6 +374,38 @@ def test_pauli_frame_normalised_programs_vs_oracle(cuda, monkeypatch, seed, n, f
         _close_grad(out["1"][1][b], orc.adjoint_grad(c, obs[0] + obs[1] * -0.7, bind)[1])
 
 
+@pytest.mark.parametrize("seed,n", [(0, 12), (1, 14), (2, 13), (3, 15)])
+def test_checkpointed_adjoint_vs_oracle(cuda, monkeypatch, seed, n):
+    """Checkpointed adjoint sweep (engine.Bound._checkpoints): forward pass outputs kept, the
+    backward passes reload psi from them.  Gradients and energies against the oracle and
+    against the store-and-uncompute sweep (QF_CKPT=0); the plan must actually use it."""
+    from circuits import pauli_rotation_circuit
+    from paper_2003_02989_b200.engine import ENGINE
+
+    rng = np.random.default_rng(700 + seed)
+    c = pauli_rotation_circuit(rng, n, 240, n_sym=6)
+    syms = circuit_symbols(c)
+    theta = rng.uniform(-3.5, 3.5, size=(4, len(syms))).astype(np.float32)
+    obs = [random_observable(rng, n, diag=True, k=6), random_observable(rng, n, diag=True, k=3)]
+    monkeypatch.setenv("QF_JIT", "1")
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("QF_CKPT", flag)
+        ENGINE._bound.clear()
+        ENGINE._plans.clear()
+        b = ENGINE.bind([c] * 4, syms, obs, want_grad=True)
+        assert bool(b.plan.extra.get("ckpt")) == (flag == "1")
+        out[flag] = ops.expectation_and_gradient([c] * 4, syms, theta, obs, upstream=np.array([[1.0, -0.7]] * 4))
+    np.testing.assert_allclose(out["1"][0], out["0"][0], atol=2e-5)
+    np.testing.assert_allclose(out["1"][1], out["0"][1], atol=5e-5, rtol=1e-5)
+    for b in range(4):
+        bind = dict(zip(syms, theta[b].astype(np.float64)))
+        ref = orc.simulate_amps(c, bind)
+        for k, o in enumerate(obs):
+            assert out["1"][0][b, k] == pytest.approx(orc.expectation(ref, o, n), abs=EXP)
+        _close_grad(out["1"][1][b], orc.adjoint_grad(c, obs[0] + obs[1] * -0.7, bind)[1])
+
+
 # ---------------------------------------------------------------------------
 # global-qubit sharding (distributed.py) on the engine
 # ---------------------------------------------------------------------------

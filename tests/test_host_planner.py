@@ -139,7 +139,8 @@ def test_frame_programs_event_invariants(adjoint):
         prog = pl.build_program(c, pl.analyse(c, si), 11, adjoint=False, observables=[obs], obs_diag_ids=[0],
                                 frame=True)
     assert prog.frame
-    ev = prog.frame_events
+    ev = np.array([e for e in prog.frame_events if int(e[0]) != pl.EV_PASS])
+    assert sum(int(e[0]) == pl.EV_PASS for e in prog.frame_events) == len(prog.passes)
     kinds = {pl.OP_DENSE1: {pl.EV_NX, pl.EV_NY, pl.EV_ABS1}, pl.OP_DENSE2: {pl.EV_ABS2, pl.EV_NP},
              pl.OP_DIAG: {pl.EV_DIAG}, pl.OP_OBS: {pl.EV_OBS}}
     assert len(ev) == len(prog.ops)
