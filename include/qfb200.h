@@ -190,6 +190,16 @@ int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int row
                        int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
                        QfFrame* frame_out, double* pass_m, int n_pass, void* stream);
 
+/* Block-fused adjoint (planner.build_program(block=True)): per (row, block) the gradient
+ * value Tr(W_f^dag G_f W_f A) of every factor f of a fused dense block from the block's
+ * two-point matrix A (slots of ``a`` [rows, n_a], reduced from the adjoint's partials).
+ * blocks [n_blocks, 4] = (factor begin, factor end, D, first A slot); factors [n_factors, 3]
+ * = (matrix offset in mats, generator offset in gens or -1, symbol column); gens: complex
+ * D x D generators (interleaved fp64); out [rows, n_factors].  Replaces the per-gate
+ * Im<lambda|G|psi> loop of the adjoint differentiator for fused blocks. */
+int qf_block_grads(const int32_t* blocks, int n_blocks, const int32_t* factors, int n_factors, const double* gens,
+                   const float* mats, int n_mat, const double* a, int n_a, double* out, int rows, void* stream);
+
 /* Generic Pauli-sum expectation partials: partials[row, k, chunk] = coef[row, k] *
  * sum_{x in chunk} Re(conj(psi[x ^ xm_k]) i^{ny_k} (-1)^{popc(x & zm_k)} psi[x]);
  * chunks = ceil(2^n / 2048).  Sum with qf_reduce_slots (slots = terms, tiles = chunks).

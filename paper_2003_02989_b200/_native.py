@@ -17,7 +17,7 @@ EXPORTS = (
     "qf_last_error", "qf_version", "qf_device_sm_count", "qf_build_ops", "qf_run_passes",
     "qf_adjoint_passes", "qf_reduce_slots", "qf_pauli_expect", "qf_pauli_apply", "qf_sample",
     "qf_jit_compile", "qf_jit_free", "qf_jit_load", "qf_jit_function", "qf_jit_unload", "qf_jit_run",
-    "qf_reduce_slots_scaled", "qf_frame_walk", "qf_jit_occupancy", "qf_frame_walk_ckpt",
+    "qf_reduce_slots_scaled", "qf_frame_walk", "qf_jit_occupancy", "qf_frame_walk_ckpt", "qf_block_grads",
 )
 
 _p = C.c_void_p
@@ -80,6 +80,7 @@ def load(build_if_missing: bool = True):
                                   _p]
     lib.qf_frame_walk_ckpt.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, C.c_int, _p, C.c_int, _p, C.c_int, _p,
                                        _p, _p, C.c_int, _p]
+    lib.qf_block_grads.argtypes = [_p, C.c_int, _p, C.c_int, _p, _p, C.c_int, _p, C.c_int, _p, C.c_int, _p]
     lib.qf_pauli_expect.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _i64, _p, _p]
     lib.qf_pauli_apply.argtypes = [_p, _p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _i64, _p]
     lib.qf_sample.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p]

@@ -541,7 +541,11 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
           N[i * D + j] = acc;
         }
       for (int i = 0; i < D * D; ++i) M[off + i] = make_float2((float)N[i].x, (float)N[i].y);
-      if (slot >= 0) slot_scale[(size_t)row * n_slots + slot] = mp == m ? m : sqrt(m * mp);  // after the apply
+      if (slot >= 0) {  // after the apply; a fused block's E[7] A slots all scale by m
+        const double sc = mp == m ? m : sqrt(m * mp);
+        const int cnt = E[7] > 0 ? E[7] : 1;
+        for (int j = 0; j < cnt; ++j) slot_scale[(size_t)row * n_slots + slot + j] = sc;
+      }
     } else if (kind == 8) {  // pass boundary (checkpointed adjoint): record / reload psi's scale
       if (pass_m) {
         if (!adjoint) pass_m[(size_t)row * n_pass + E[6]] = m;
@@ -721,6 +725,81 @@ int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int row
       events, n_events, adjoint, rows, reinterpret_cast<float2*>(mats), n_mat, angles, n_ang, slot_scale, n_slots,
       frame_in, frame_out, pass_m, n_pass);
   return check_launch("frame_walk_global_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Block-fused adjoint: gradients of the factors of a fused dense block from the block's
+// two-point matrix A = (rho - rho^dag)/2i, rho[j][k] = sum psi_in[j] conj(lam_in[k]) taken at
+// the block's input by the adjoint pass (planner.build_program(block=True)).  With W_f the
+// product of the block's first f factors (forward order) and G_f = 2 coeff G (non-identity
+// part), factor f's value is Im<lam_f|G_f|psi_f> = Tr(W_f^dag G_f W_f A).  A slots per block:
+// D diagonal entries A[j][j], then 2 Re A[j][k], 2 Im A[j][k] for j < k.  One thread per
+// (row, block), fp64.
+// ---------------------------------------------------------------------------
+__global__ void block_grads_kernel(const int32_t* __restrict__ blocks, int n_blocks,
+                                   const int32_t* __restrict__ factors, const double* __restrict__ gens,
+                                   const float2* __restrict__ mats, int n_mat, const double* __restrict__ a, int n_a,
+                                   double* __restrict__ out, int n_factors, int rows) {
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid >= (int64_t)rows * n_blocks) return;
+  const int row = (int)(tid / n_blocks), b = (int)(tid % n_blocks);
+  const int fb = blocks[b * 4], fe = blocks[b * 4 + 1], D = blocks[b * 4 + 2], slot0 = blocks[b * 4 + 3];
+  const double* A = a + (size_t)row * n_a + slot0;
+  const float2* M = mats + (size_t)row * n_mat;
+  Z W[16], T[16];
+  for (int i = 0; i < D; ++i)
+    for (int j = 0; j < D; ++j) W[i * D + j] = {i == j ? 1.0 : 0.0, 0.0};
+  for (int f = fb; f < fe; ++f) {
+    const int moff = factors[f * 3], goff = factors[f * 3 + 1];
+    for (int i = 0; i < D; ++i)  // W <- M_f W
+      for (int j = 0; j < D; ++j) {
+        Z acc{0, 0};
+        for (int k = 0; k < D; ++k) {
+          const float2 m = M[moff + i * D + k];
+          acc = zadd(acc, zmul(Z{m.x, m.y}, W[k * D + j]));
+        }
+        T[i * D + j] = acc;
+      }
+    for (int i = 0; i < D * D; ++i) W[i] = T[i];
+    if (goff < 0) {
+      out[(size_t)row * n_factors + f] = 0.0;
+      continue;
+    }
+    const double* G = gens + (size_t)goff * 2;
+    for (int i = 0; i < D; ++i)  // T = G W
+      for (int j = 0; j < D; ++j) {
+        Z acc{0, 0};
+        for (int k = 0; k < D; ++k) acc = zadd(acc, zmul(Z{G[(i * D + k) * 2], G[(i * D + k) * 2 + 1]}, W[k * D + j]));
+        T[i * D + j] = acc;
+      }
+    // K[r][c] = sum_i conj(W[i][r]) T[i][c]; value = sum_j Re K[j][j] A_jj
+    //   + sum_{j<k} (Re K[k][j] * 2Re A_jk - Im K[k][j] * 2Im A_jk)
+    double val = 0.0;
+    int e = D;
+    for (int j = 0; j < D; ++j) {
+      for (int k = j; k < D; ++k) {
+        Z acc{0, 0};
+        for (int i = 0; i < D; ++i) acc = zadd(acc, zmul(Z{W[i * D + k].x, -W[i * D + k].y}, T[i * D + j]));
+        if (k == j) {
+          val += acc.x * A[j];
+        } else {
+          val += acc.x * A[e] - acc.y * A[e + 1];
+          e += 2;
+        }
+      }
+    }
+    out[(size_t)row * n_factors + f] = val;
+  }
+}
+
+int qf_block_grads(const int32_t* blocks, int n_blocks, const int32_t* factors, int n_factors, const double* gens,
+                   const float* mats, int n_mat, const double* a, int n_a, double* out, int rows, void* stream) {
+  if (rows == 0 || n_blocks == 0) return 0;
+  const int64_t n = (int64_t)rows * n_blocks;
+  const int T = 128;
+  block_grads_kernel<<<(unsigned)((n + T - 1) / T), T, 0, (cudaStream_t)stream>>>(
+      blocks, n_blocks, factors, gens, reinterpret_cast<const float2*>(mats), n_mat, a, n_a, out, n_factors, rows);
+  return check_launch("block_grads_kernel");
 }
 
 int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, float* mats, int n_mat,

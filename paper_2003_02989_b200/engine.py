@@ -28,6 +28,16 @@ def _require_cuda(device=None) -> torch.device:
     return dev
 
 
+_TOTAL_MEM: dict = {}
+
+
+def _total_memory(device) -> int:
+    idx = device.index or 0
+    if idx not in _TOTAL_MEM:
+        _TOTAL_MEM[idx] = torch.cuda.get_device_properties(idx).total_memory
+    return _TOTAL_MEM[idx]
+
+
 def _ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
@@ -76,6 +86,24 @@ class DeviceProgram:
         ev = prog.frame_events if prog.frame_events is not None else np.zeros((0, pl.EV_INTS), np.int32)
         self.n_events = int(ev.shape[0])
         self.t_events = up(ev.reshape(-1), torch.int32)
+        # block-fused adjoint: A slots reduced into consecutive columns, one range per block
+        blk = prog.blocks if prog.blocks is not None else np.zeros((0, 4), np.int32)
+        self.n_blocks = int(blk.shape[0])
+        if self.n_blocks:
+            blk = blk.copy()
+            amap, col = {}, 0
+            for i in range(self.n_blocks):
+                D, slot0 = int(blk[i, 2]), int(blk[i, 3])
+                for e in range(pl.block_slots(D)):
+                    amap[col + e] = [slot0 + e]
+                blk[i, 3] = col
+                col += pl.block_slots(D)
+            self.n_acols = col
+            self.acsr = self.csr(amap, col)
+            self.t_blocks = up(blk.reshape(-1), torch.int32)
+            self.t_bfac = up(prog.block_factors.reshape(-1), torch.int32)
+            self.t_bgen = up(prog.block_gens, torch.float64)
+            self.n_bfac = int(prog.block_factors.shape[0])
 
     def recipe(self, fixed_t, fixed_rows, const_t, const_rows) -> nat.QfBuildRecipe:
         a = self.r_arrays
@@ -219,8 +247,12 @@ class Bound:
                  and _jit.enabled(len(self.circuits), max(n, pl.N_MIN)))
         over = pl.batch_overrides(template, self.circuits, sym_index, pl.analyse(template, sym_index)) \
             if len(self.circuits) > 1 else {}
+        # block-fused adjoint (planner.build_ops(block=True)): plan-specialised kernels only
+        block = (want_grad and os.environ.get("QF_BLOCK_ADJ", "1") not in ("0", "", "false")
+                 and _jit.enabled(len(self.circuits), max(n, pl.N_MIN)))
         self.plan = engine.plan(template, sym_index, obs, want_grad, self.lam_diag,
-                                tuple(self.hkeys) if want_grad else None, device, from_state, frame, over)
+                                tuple(self.hkeys) if want_grad else None, device, from_state, frame, over,
+                                block=block)
         plan = self.plan
         self.frame = plan.fwd.frame
 
@@ -264,6 +296,12 @@ class Bound:
         if want_grad:
             ad = plan.adj
             self.grad_csr = ad.csr(ad.prog.grad_slots, self.S)
+            if ad.n_blocks:
+                fmap: dict = {}
+                for f, sym in enumerate(ad.prog.block_factors[:, 2].tolist()):
+                    if sym >= 0:
+                        fmap.setdefault(sym, []).append(f)
+                self.block_csr = ad.csr(fmap, self.S)
             self.energy_csr = ad.csr({0: ad.prog.energy_slots}, 1)
             if not self.lam_diag and self.hkeys:
                 xs, zs, ys = [], [], []
@@ -378,9 +416,13 @@ class Bound:
         if fw.jit(self.device, self.B) is None or plan.adj.jit(self.device, self.B) is None:
             return None
         need = (P - 1) * psi.numel() * psi.element_size()
-        if need > 0.4 * torch.cuda.mem_get_info(self.device)[0]:
+        # a static budget: cudaMemGetInfo stalls for up to tens of ms while kernels run
+        if need > 0.3 * _total_memory(self.device):
             return None
-        ck = [torch.empty_like(psi) for _ in range(P - 1)] + [psi]
+        try:
+            ck = [torch.empty_like(psi) for _ in range(P - 1)] + [psi]
+        except torch.cuda.OutOfMemoryError:
+            return None
         return ck, torch.empty((self.B, P), dtype=torch.float64, device=self.device)
 
     def _adjoint(self, lib, psi, theta, upstream, stream, out, frame_f=None, ckpt=None):
@@ -417,7 +459,7 @@ class Bound:
             else:
                 lam.zero_()
         partials = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
-        ja = ad.jit(dev, B)
+        ja = ad.jit(dev, B, force=ad.n_blocks > 0)
         if ckpt:
             ck = ckpt[0]
             ja.run_ckpt(B, [_ptr(t) for t in reversed(ck)], None, _ptr(lam), _ptr(mats), _ptr(angs), _ptr(hw_t),
@@ -436,6 +478,18 @@ class Bound:
             ptr, lst = self.grad_csr
             nat.check(lib.qf_reduce_slots_scaled(_ptr(partials), B, ad.prog.n_slots, ad.tiles, _ptr(ptr), _ptr(lst),
                                                  self.S, _ptr(grad), 0, _ptr(scale), stream))
+        if ad.n_blocks and self.S:
+            # fused blocks: reduce each block's A matrix, then every factor's gradient from it
+            acols = torch.empty((B, ad.n_acols), dtype=torch.float64, device=dev)
+            ptr, lst = ad.acsr
+            nat.check(lib.qf_reduce_slots_scaled(_ptr(partials), B, ad.prog.n_slots, ad.tiles, _ptr(ptr), _ptr(lst),
+                                                 ad.n_acols, _ptr(acols), 0, _ptr(scale), stream))
+            vals = torch.empty((B, ad.n_bfac), dtype=torch.float64, device=dev)
+            nat.check(lib.qf_block_grads(_ptr(ad.t_blocks), ad.n_blocks, _ptr(ad.t_bfac), ad.n_bfac, _ptr(ad.t_bgen),
+                                         _ptr(mats), ad.prog.n_mat, _ptr(acols), ad.n_acols, _ptr(vals), B, stream))
+            ptr, lst = self.block_csr
+            nat.check(lib.qf_reduce_slots(_ptr(vals), B, ad.n_bfac, 1, _ptr(ptr), _ptr(lst), self.S, _ptr(grad), 1,
+                                          stream))
         if self.lam_diag:
             energy = torch.empty((B, 1), dtype=torch.float64, device=dev)
             ptr, lst = self.energy_csr
@@ -453,11 +507,11 @@ class Engine:
         self._lock = threading.Lock()
 
     def plan(self, template, symbol_index, obs: ObsInfo, adjoint: bool, lam_diag: bool, hkeys, device,
-             from_state: bool = False, frame: bool = False, overrides=None):
+             from_state: bool = False, frame: bool = False, overrides=None, block: bool = False):
         overrides = overrides or {}
         topo = pl.topology_key(template, symbol_index)
         key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state, frame,
-               tuple(sorted(overrides.items())), pl.FUSION_ENABLED)
+               tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block)
         with self._lock:
             hit = self._plans.get(key)
         if hit is not None:
@@ -475,12 +529,13 @@ class Engine:
             infos_a = pl.analyse(template, symbol_index, overrides)
             hterms = _TermList([_Term(dict(kk), 1.0) for kk in hkeys])
             adjp = pl.build_program(template, infos_a, n_eff, adjoint=True, observables=[hterms],
-                                    lam_diag=lam_diag, frame=frame)
+                                    lam_diag=lam_diag, frame=frame, block=block)
         ckpt = False
         if adjp is not None and frame and lam_diag and not from_state and \
                 os.environ.get("QF_CKPT", "1") not in ("0", "", "false"):
             fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
-                                   obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame, mirror=True)
+                                   obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame, mirror=True,
+                                   block=block)
             # the adjoint's backward pass i must undo exactly forward pass P-1-i (both lists
             # are in forward order), and both frame walks must hold the same Pauli frame at every
             # pass boundary: true for normalised rotations and diagonal ops, not for general

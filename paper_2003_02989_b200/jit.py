@@ -100,6 +100,25 @@ def _int_poly(prog, tb: int, te: int):
     return (base, ms, H) if H <= 255 else None
 
 
+def _int_grad(prog, tb: int, te: int, ms: list):
+    """Gradient weights of an integer-weight phase polynomial: (wb, idm) with every
+    non-identity term's weight w_k = wb * m_k, and idm = the identity terms' total multiple
+    (their weight is 0: subtracted from h); None when the weights are not of that form."""
+    wb, idm = None, 0
+    for kk, m in zip(range(tb, te), ms):
+        w_ = float(prog.term_w[kk])
+        if int(prog.term_mask[kk]) == 0:
+            if w_ != 0.0:
+                return None
+            idm += m
+            continue
+        if wb is None:
+            wb = w_ / m
+        elif abs(w_ - wb * m) > 1e-6 * max(1.0, abs(w_)):
+            return None
+    return (0.0 if wb is None else wb), idm
+
+
 def _wht_code(vals: dict, R: int, kind: str, out: str, indent: str) -> list:
     """Walsh-Hadamard transform over 2^R entries with symbolic zero tracking.
     vals: S -> variable name (entries absent are zero).  Emits `out{r}` variables."""
@@ -129,6 +148,24 @@ def _wht_code(vals: dict, R: int, kind: str, out: str, indent: str) -> list:
     zero = {"u32": "0u", "int": "0"}.get(kind, "0.f")
     for r in range(1 << R):
         lines.append(f"{indent}const {kind} {out}{r} = {cur.get(r, zero)};")
+    return lines
+
+
+def _block_code(D: int, mhi: int, mlo: int, slot_rel: int, gs_store, indent: str, NR: int) -> list:
+    """Block-fused adjoint op: after U^dag, the thread's share of the block's two-point matrix
+    A = (rho - rho^dag) / 2i, rho[j][k] = sum psi_j conj(lam_k) over the other qubits: D
+    diagonal entries, then Re / Im of 2 A[j][k] for j < k (planner.block_slots order).
+    Local index bit 1 is register mask ``mhi`` (D = 4), bit 0 ``mlo``."""
+    lines = []
+    e = 0
+    for j in range(D):
+        lines.append(indent + gs_store(slot_rel + e, f"blk_entry<{NR}, {mhi}, {mlo}, {j}, {j}, 0>(v0, v1)"))
+        e += 1
+    for j in range(D):
+        for k in range(j + 1, D):
+            for part in (1, 2):
+                lines.append(indent + gs_store(slot_rel + e, f"blk_entry<{NR}, {mhi}, {mlo}, {j}, {k}, {part}>(v0, v1)"))
+                e += 1
     return lines
 
 
@@ -191,6 +228,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     continue
                 ip = _int_poly(prog, int(op_[4]), int(op_[5]))
                 if ip is None or ip[0] < ab or ip[0] >= ae:
+                    continue
+                if adj and int(op_[7]) >= 0 and _int_grad(prog, int(op_[4]), int(op_[5]), ip[1]) is None:
                     continue
                 int_tables[k_] = (ip, tbl_bytes)
                 tbl_bytes += (2 * ip[2] + 1) * 16
@@ -484,7 +523,9 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                         if adj:
                             w(f"      apply1<{s0}, {NR}, {cls}>(v1, u00, u01, u10, u11);")
                         w(f"      apply1<{s0}, {NR}, {cls}>(v0, u00, u01, u10, u11);")
-                    if adj and slot >= 0:
+                    if adj and slot >= 0 and int(op[13]):
+                        o.extend(_block_code(2, 0, 1 << s0, slot - slb, gs_store, "      ", NR))
+                    elif adj and slot >= 0:
                         g0 = int(op[8])
                         if gk:
                             sc = float(gm[g0 + 4, 0])
@@ -509,7 +550,9 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                         w("    {")
                         w(f"      apply2m<{s0}, {s1}, {NR}>(v0, M + {moff}, MN + {moff});"
                           f" apply2m<{s0}, {s1}, {NR}>(v1, M + {moff}, MN + {moff});")
-                        if slot >= 0:
+                        if slot >= 0 and int(op[13]):
+                            o.extend(_block_code(4, 1 << s0, 1 << s1, slot - slb, gs_store, "      ", NR))
+                        elif slot >= 0:
                             g0 = int(op[8])
                             gl = ", ".join(f"make_float2({_flit(gm[g0 + i, 0])}, {_flit(gm[g0 + i, 1])})"
                                            for i in range(16))
@@ -563,10 +606,11 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                                 w(f"      {pre}h{S} += (__popc({gv} & {m}u) & 1) ? {-mk} : {mk};")
                         o.extend(_wht_code({S: f"{pre}h{S}" for S in groups}, R, "int", f"{pre}H", "      "))
                         if adj and slot >= 0:
-                            wb = float(prog.term_w[tb + ms.index(min(ms, key=abs))]) / min(ms, key=abs)
+                            wb, idm = _int_grad(prog, tb, te, ms)
                             w("      float gq = 0.f;")
                             for r in range(NR):
-                                w(f"      gq = fmaf((float){pre}H{r}, im_conj_mul(v1[{r}], v0[{r}]), gq);")
+                                hr = f"{pre}H{r}" if not idm else f"({pre}H{r} - {idm})"
+                                w(f"      gq = fmaf((float){hr}, im_conj_mul(v1[{r}], v0[{r}]), gq);")
                             w("      " + gs_store(slot - slb, f"{_flit(wb)} * gq"))
                         for r in range(NR):
                             w(f"      {{ const float4 T = TB[{off // 16 + H} + {pre}H{r}];"

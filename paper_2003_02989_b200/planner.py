@@ -284,11 +284,17 @@ def _diag_op_qubits(gates, infos):
 FUSION_ENABLED = True   # False: one op per gate (the reference's fuse_enabled=False cells)
 
 
-def build_ops(infos: list[GateInfo], adjoint: bool) -> list[Op]:
+def build_ops(infos: list[GateInfo], adjoint: bool, block: bool = False) -> list[Op]:
     """Fuse gates into dense 1q/2q ops and diagonal phase-polynomial ops.
 
     ``adjoint``: symbolic gates are never merged with anything except that
     symbolic diagonal gates sharing one symbol share a DIAG op.
+
+    ``block`` (adjoint only): symbolic gates are fused into dense blocks like in the forward
+    program -- a symbolic diagonal gate joins the dense op that is the last op on all its
+    qubits -- and the adjoint takes every factor's gradient from the block's reduced
+    two-point matrix (see build_program / qf_block_grads).  Diagonal gates that do not land on
+    a dense op keep the phase-polynomial path (QAOA cost layers stay DIAG ops).
     """
     if not FUSION_ENABLED:
         out = []
@@ -309,6 +315,14 @@ def build_ops(infos: list[GateInfo], adjoint: bool) -> list[Op]:
 
     for gi, info in enumerate(infos):
         tq = info.targets
+        if info.diag and block and info.symbolic:
+            js = {last.get(q) for q in tq}
+            j = js.pop() if len(js) == 1 else None
+            if j is not None and ops[j] is not None and ops[j].kind in (OP_DENSE1, OP_DENSE2) \
+                    and set(tq) <= set(ops[j].qubits):
+                ops[j].factors.append(gi)   # j is the last op on every target: exact
+                ops[j].symbolic = True
+                continue
         if info.diag:
             # walk back over ops that commute with this gate (disjoint or diagonal)
             # and join the most recent compatible DIAG op
@@ -342,7 +356,7 @@ def build_ops(infos: list[GateInfo], adjoint: bool) -> list[Op]:
                     last[q] = len(ops) - 1
             continue
 
-        can_merge_sym = not adjoint
+        can_merge_sym = (not adjoint) or block
         if len(tq) == 1:
             q = tq[0]
             j = last.get(q)
@@ -380,9 +394,39 @@ def build_ops(infos: list[GateInfo], adjoint: bool) -> list[Op]:
         last[a] = last[b] = len(ops) - 1
 
     out = [o for o in ops if o is not None]
+    if block:
+        out = _split_small_blocks(out, infos)
     for i, o in enumerate(out):
         o.index = i
     return out
+
+
+BLOCK_MIN_SYMBOLIC = 3
+
+
+def _split_small_blocks(ops: list, infos) -> list:
+    """Keep a fused symbolic block only where it pays: a two-qubit block with at least
+    BLOCK_MIN_SYMBOLIC symbolic factors (one dense 4x4 apply and a 16-entry A matrix instead
+    of a per-gate sweep).  Smaller blocks -- and every one-qubit run, whose per-gate
+    normalised rotations are as cheap and keep the Pauli frame and the checkpointed adjoint
+    available -- go back to one op per gate, in place (exact: a merged gate was the last op
+    on its qubits)."""
+    res = []
+    for o in ops:
+        nsym = sum(infos[gi].symbolic for gi in o.factors)
+        if o.kind in (OP_DENSE1, OP_DENSE2) and o.symbolic and len(o.factors) > 1 and \
+                not (o.kind == OP_DENSE2 and nsym >= BLOCK_MIN_SYMBOLIC):
+            for gi in o.factors:
+                inf = infos[gi]
+                sym = inf.sym if inf.symbolic else -1
+                if inf.diag:
+                    res.append(Op(OP_DIAG, tuple(sorted(inf.targets)), gates=[gi], symbolic=inf.symbolic, sym=sym))
+                else:
+                    res.append(Op(OP_DENSE1 if len(inf.targets) == 1 else OP_DENSE2, tuple(inf.targets),
+                                  factors=[gi], symbolic=inf.symbolic, sym=sym))
+        else:
+            res.append(o)
+    return res
 
 
 def dependencies(ops: list[Op]) -> list[set]:
@@ -623,6 +667,12 @@ class Program:
     stats: dict
     frame: bool = False
     frame_events: np.ndarray = None   # [E, EV_INTS] int32, execution order
+    # block-fused adjoint (build_ops(block=True)): per block [factor begin, factor end, D,
+    # first A slot]; per factor [mat offset, generator offset (-1: fixed), symbol column];
+    # block_gens: complex D x D generators 2 coeff G (non-identity part), interleaved float64
+    blocks: np.ndarray = None
+    block_factors: np.ndarray = None
+    block_gens: np.ndarray = None
 
 
 def _bit_subset(mask: int, reg_glob: list) -> int:
@@ -649,6 +699,7 @@ class Emitter:
         self.obs_slots: dict = {}
         self.energy_slots: list = []
         self.coef_cols = []       # (obs id, term index within observable)
+        self.blocks = []          # (factor gate indices, order, D, first A slot)
 
     # -- per-row matrix slab --------------------------------------------------
     def dense_mat(self, op: Op, order: tuple) -> int:
@@ -751,9 +802,15 @@ def frame_eligible(ops: list[Op], infos, adjoint: bool) -> bool:
     return True
 
 
+def block_slots(D: int) -> int:
+    """A slots of a D x D block: D diagonal entries + Re/Im of the D(D-1)/2 upper ones."""
+    return D * D
+
+
 def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool,
                   observables=None, obs_diag_ids=(), lam_diag: bool = False,
-                  from_state: bool = False, frame: bool = False, mirror: bool = False) -> Program:
+                  from_state: bool = False, frame: bool = False, mirror: bool = False,
+                  block: bool = False) -> Program:
     """Plan + emit.  ``observables``: list of PauliSums; ``obs_diag_ids``: those fused as
     OBS ops at the end of the forward program; ``lam_diag``: adjoint with a diagonal H
     whose lambda-init / energy is fused into the first backward pass; ``from_state``:
@@ -768,7 +825,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     # mirror: a forward program with exactly the adjoint program's ops and tile passes (no
     # symbolic fusion, adjoint tile size), so its pass outputs are checkpoints the adjoint
     # sweep can read and both Pauli-frame walks agree at every pass boundary
-    ops = build_ops(infos, adjoint or mirror)
+    # a mirror program takes the block-mode op list too (same ops per pass as the adjoint)
+    block = block and (adjoint or mirror)
+    ops = build_ops(infos, adjoint or mirror, block=block)
     L, R = geometry(adjoint)
     if mirror:
         L = geometry(True)[0]
@@ -875,6 +934,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         order = (a, b) if slot_of[a] < slot_of[b] else (b, a)
                         orow[1], orow[2] = slot_of[order[0]], slot_of[order[1]]
                     orow[3] = em.dense_mat(op, order)
+                    is_block = adjoint and op.symbolic and len(op.factors) > 1
                     if op.kind == OP_DENSE1:
                         cl = {infos[gi].cls for gi in op.factors}
                         orow[9] = cl.pop() if len(cl) == 1 else CLS_GENERAL
@@ -884,10 +944,12 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         elif frame and orow[9] == CLS_XLIKE:
                             orow[9] = CLS_GENERAL   # an absorbed X frame breaks the X-like structure
                                                     # (real matrices stay real under X^a Z^b)
+                        if is_block:
+                            orow[9] = CLS_GENERAL   # the A matrix is taken frame-free after U^dag
                     else:
                         orow[9] = CLS_GENERAL
                         if frame and len(op.factors) == 1 and infos[op.factors[0]].symbolic and \
-                                infos[op.factors[0]].pstring:
+                                infos[op.factors[0]].pstring and not is_block:
                             orow[9] = CLS_NP
                     ev = None
                     if frame:
@@ -901,7 +963,14 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                             ev = [EV_NP, order[0], order[1], int(orow[3]), -1, -1, code, 0]
                         else:
                             ev = [EV_ABS2, order[0], order[1], int(orow[3]), -1, -1, 0, 0]
-                    if adjoint and op.symbolic:
+                    if is_block:
+                        D = 1 << len(order)
+                        orow[7] = em.n_slots
+                        for _ in range(block_slots(D)):
+                            em.new_slot()
+                        orow[13] = D
+                        em.blocks.append((list(op.factors), order, D, int(orow[7])))
+                    elif adjoint and op.symbolic:
                         (gi,) = op.factors
                         info = infos[gi]
                         gm, _ = generator_matrix_from_terms(info.terms, order)
@@ -917,6 +986,8 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         em.grad_slots.setdefault(info.sym, []).append(int(orow[7]))
                     if ev is not None:
                         ev[4] = int(orow[7])
+                        if is_block:
+                            ev[7] = block_slots(1 << len(order))   # slots sharing the scale m
                         events.append(ev)
                 elif op.kind == OP_DIAG:
                     terms = em.diag_terms(op)
@@ -961,6 +1032,24 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         prow[81] = len(em.grp)
         prow[83] = len(em.op_rows)
         em.pass_rows.append(prow)
+
+    # block-fused adjoint: one matrix per factor (embedded in the block's basis), allocated
+    # after every pass's range so the pass kernels never stage them
+    blocks, bfac, bgen = [], [], []
+    for factors, order, D, slot0 in em.blocks:
+        fb = len(bfac)
+        for gi in factors:
+            info = infos[gi]
+            moff = em.dense_mat(Op(OP_DENSE1 if D == 2 else OP_DENSE2, tuple(order), factors=[gi]), order)
+            goff, sym = -1, -1
+            if info.symbolic:
+                gm, _ = generator_matrix_from_terms(info.terms, order)
+                gm = gm * (2.0 * info.coeff)
+                goff = len(bgen) // 2
+                bgen.extend(np.stack([gm.real, gm.imag], -1).reshape(-1).tolist())
+                sym = info.sym
+            bfac.append((moff, goff, sym))
+        blocks.append((fb, len(bfac), D, slot0))
 
     # build recipe arrays
     gen_sym = np.array([g.sym for g in gen_rows], dtype=np.int32)
@@ -1014,6 +1103,9 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         recipe=recipe, grad_slots=em.grad_slots, obs_slots=em.obs_slots,
         energy_slots=em.energy_slots, stats=stats, frame=frame,
         frame_events=np.array(events, dtype=np.int32).reshape(-1, EV_INTS),
+        blocks=np.array(blocks, dtype=np.int32).reshape(-1, 4),
+        block_factors=np.array(bfac, dtype=np.int32).reshape(-1, 3),
+        block_gens=np.array(bgen, dtype=np.float64),
     )
 
 

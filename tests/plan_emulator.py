@@ -159,6 +159,11 @@ def run_adjoint(prog: pl.Program, mats, angs, B, n, psi, lam, hcoefs):
                         qs = [reg_glob[o[1]]] if o[0] == pl.OP_DENSE1 else [reg_glob[o[1]], reg_glob[o[2]]]
                         d = 1 << len(qs)
                         u = mats[b, o[3]:o[3] + d * d].reshape(d, d)
+                        if o[13]:   # fused block: U^dag, then the two-point matrix A (slots)
+                            psi[b] = _apply(psi[b], u.conj().T, qs, n)
+                            lam[b] = _apply(lam[b], u.conj().T, qs, n)
+                            slots[b, o[7]:o[7] + d * d] += _block_a(psi[b], lam[b], qs, n)
+                            continue
                         if o[7] >= 0:
                             g = gm[o[8]:o[8] + d * d].reshape(d, d)
                             slots[b, o[7]] += float(np.vdot(lam[b], _apply(psi[b], g, qs, n)).imag)
@@ -183,6 +188,47 @@ def run_adjoint(prog: pl.Program, mats, angs, B, n, psi, lam, hcoefs):
                         lam[b] = h * psi[b]
                         slots[b, o[7]] += float(np.sum(np.abs(psi[b]) ** 2 * h))
     return slots
+
+
+def _block_a(psi, lam, qs, n):
+    """A = (rho - rho^dag)/2i, rho[j][k] = sum psi_j conj(lam_k), in qf_block_grads' slot
+    order (diagonal, then 2 Re / 2 Im of the upper entries)."""
+    d = 1 << len(qs)
+    p = np.moveaxis(psi.reshape((2,) * n), [n - 1 - q for q in qs], list(range(len(qs)))).reshape(d, -1)
+    l = np.moveaxis(lam.reshape((2,) * n), [n - 1 - q for q in qs], list(range(len(qs)))).reshape(d, -1)
+    rho = p @ l.conj().T
+    A = (rho - rho.conj().T) / 2j
+    out = [A[j, j].real for j in range(d)]
+    for j in range(d):
+        for k in range(j + 1, d):
+            out += [2 * A[j, k].real, 2 * A[j, k].imag]
+    return np.array(out)
+
+
+def block_grads(prog: pl.Program, mats, a_slots, n_cols):
+    """NumPy restatement of qf_block_grads: per factor Tr(W^dag G W A), summed per symbol."""
+    B = a_slots.shape[0]
+    out = np.zeros((B, n_cols))
+    gens = prog.block_gens.reshape(-1, 2)
+    gens = gens[:, 0] + 1j * gens[:, 1]
+    for b in range(B):
+        for fb, fe, D, slot0 in prog.blocks:
+            a = a_slots[b, slot0:slot0 + D * D]
+            A = np.zeros((D, D), dtype=np.complex128)
+            e = D
+            for j in range(D):
+                A[j, j] = a[j]
+                for k in range(j + 1, D):
+                    A[j, k] = (a[e] + 1j * a[e + 1]) / 2
+                    A[k, j] = np.conj(A[j, k])
+                    e += 2
+            W = np.eye(D, dtype=np.complex128)
+            for moff, goff, sym in prog.block_factors[fb:fe]:
+                W = mats[b, moff:moff + D * D].reshape(D, D) @ W
+                if goff >= 0:
+                    G = gens[goff:goff + D * D].reshape(D, D)
+                    out[b, sym] += float(np.trace(W.conj().T @ G @ W @ A).real)
+    return out
 
 
 def slots_to_cols(slots, mapping, n_cols):

@@ -406,6 +406,34 @@ def test_checkpointed_adjoint_vs_oracle(cuda, monkeypatch, seed, n):
         _close_grad(out["1"][1][b], orc.adjoint_grad(c, obs[0] + obs[1] * -0.7, bind)[1])
 
 
+@pytest.mark.parametrize("seed,n,diag", [(0, 9, True), (1, 12, True), (2, 11, False), (3, 13, True)])
+def test_block_fused_adjoint_vs_oracle(cuda, monkeypatch, seed, n, diag):
+    """Block-fused adjoint (planner.build_ops(block=True), qf_block_grads): symbolic gates
+    fused into dense blocks, every factor's gradient from the block's two-point matrix.
+    Against the oracle and against the per-gate sweep (QF_BLOCK_ADJ=0), with Pauli frames
+    (diagonal observables) and without (an X/Y observable term)."""
+    from paper_2003_02989_b200.engine import ENGINE
+
+    rng = np.random.default_rng(900 + seed)
+    c = random_circuit(rng, n, 260, n_sym=7, p2=0.45)
+    syms = circuit_symbols(c)
+    theta = rng.uniform(-2.5, 2.5, size=(4, len(syms))).astype(np.float32)
+    obs = [random_observable(rng, n, diag=diag, k=5), random_observable(rng, n, diag=True, k=3)]
+    monkeypatch.setenv("QF_JIT", "1")
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("QF_BLOCK_ADJ", flag)
+        ENGINE._bound.clear()
+        b = ENGINE.bind([c] * 4, syms, obs, want_grad=True)
+        assert (b.plan.adj.n_blocks > 0) == (flag == "1")
+        out[flag] = ops.expectation_and_gradient([c] * 4, syms, theta, obs, upstream=np.array([[0.8, -1.1]] * 4))
+    np.testing.assert_allclose(out["1"][0], out["0"][0], atol=2e-5)
+    np.testing.assert_allclose(out["1"][1], out["0"][1], atol=5e-5, rtol=1e-5)
+    for b in range(4):
+        bind = dict(zip(syms, theta[b].astype(np.float64)))
+        _close_grad(out["1"][1][b], orc.adjoint_grad(c, obs[0] * 0.8 + obs[1] * -1.1, bind)[1])
+
+
 # ---------------------------------------------------------------------------
 # global-qubit sharding (distributed.py) on the engine
 # ---------------------------------------------------------------------------

@@ -51,7 +51,7 @@ def test_workload_recipes_match_reference_built_circuits(golden):
     assert json.loads(to_json(wl.brickwork_circuit(10, 6, seed=401))) == json.loads(cfg["rcs"]["circuit"])
 
 
-def _check_program(circ, obs, n, theta, adjoint_obs_diag=True):
+def _check_program(circ, obs, n, theta, adjoint_obs_diag=True, block=False):
     syms = circuit_symbols(circ)
     si = {s: i for i, s in enumerate(syms)}
     infos = pl.analyse(circ, si)
@@ -74,12 +74,15 @@ def _check_program(circ, obs, n, theta, adjoint_obs_diag=True):
     if not syms or not diag:
         return prog
     infos_a = pl.analyse(circ, si)
-    adj = pl.build_program(circ, infos_a, n, adjoint=True, observables=[nonid], lam_diag=True)
+    adj = pl.build_program(circ, infos_a, n, adjoint=True, observables=[nonid], lam_diag=True, block=block)
     em.check_invariants(adj)
     fixed, consts = pl.concrete_tables([circ], infos_a)
     mats_a, angs_a = em.build_tables(adj, theta, fixed, consts)
     sl = em.run_adjoint(adj, mats_a, angs_a, theta.shape[0], n, psi, None, np.tile(coefs, (theta.shape[0], 1)))
     grads = em.slots_to_cols(sl, adj.grad_slots, len(syms))
+    if block:
+        assert len(adj.blocks) > 0
+        grads = grads + em.block_grads(adj, mats_a, sl, len(syms))
     for b in range(theta.shape[0]):
         _, g = orc.adjoint_grad(circ, obs, dict(zip(syms, theta[b])))
         np.testing.assert_allclose(grads[b], g, atol=1e-5)  # float32 generator weights in the program
@@ -157,3 +160,16 @@ def test_frame_programs_event_invariants(adjoint):
             assert prog.recipe["term_src"].reshape(-1, 2)[int(op[11])][0] == 2
     if adjoint:
         assert any(int(e[0]) == pl.EV_NP for e in ev)        # pauli_pair_pow X/Y couplings
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_block_fused_adjoint_emulated_vs_oracle(n):
+    """Block-fused adjoint programs (planner.build_ops(block=True)) on the emulator: the
+    two-point matrices A and the per-factor traces of qf_block_grads give the oracle's
+    gradients (QCNN: conv blocks of 15 symbolic gates incl. a ZZ pair, ring-closed bricks)."""
+    phis, _, params = wl.qcnn_data(2, n)
+    model = wl.qcnn_model(n)
+    circ = Circuit(n, list(wl.qcnn_data_circuit(phis[0]).gates) + list(model.gates))
+    theta = params[:1, :len(circuit_symbols(circ))].astype(np.float64)
+    obs = PauliSum([PauliString(1.0, {n - 1: "Z"}), PauliString(0.3, {0: "Z", 1: "Z"})])
+    _check_program(circ, obs, max(n, pl.N_MIN), theta, block=True)
