@@ -736,6 +736,60 @@ int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int row
 // D diagonal entries A[j][j], then 2 Re A[j][k], 2 Im A[j][k] for j < k.  One thread per
 // (row, block), fp64.
 // ---------------------------------------------------------------------------
+extern "C++" {
+template <int D>
+__device__ __forceinline__ void block_grads_row(int fb, int fe, int slot0, int row, const int32_t* __restrict__ factors,
+                                                const double* __restrict__ gens, const float2* __restrict__ mats,
+                                                int n_mat, const double* __restrict__ a, int n_a,
+                                                double* __restrict__ out, int n_factors) {
+  const double* A = a + (size_t)row * n_a + slot0;
+  const float2* M = mats + (size_t)row * n_mat;
+  // Tr(W^dag G W A) = Tr(G B) with B = W A W^dag, carried factor by factor: B <- M_f B M_f^dag
+  Z Bm[D * D], T[D * D];
+  {
+    int e = D;
+    for (int j = 0; j < D; ++j) {
+      Bm[j * D + j] = {A[j], 0.0};
+      for (int k = j + 1; k < D; ++k) {
+        Bm[j * D + k] = {0.5 * A[e], 0.5 * A[e + 1]};
+        Bm[k * D + j] = {0.5 * A[e], -0.5 * A[e + 1]};
+        e += 2;
+      }
+    }
+  }
+  for (int f = fb; f < fe; ++f) {
+    const int moff = factors[f * 3], goff = factors[f * 3 + 1];
+    for (int i = 0; i < D; ++i)  // T = M B
+      for (int j = 0; j < D; ++j) {
+        Z acc{0, 0};
+        for (int k = 0; k < D; ++k) {
+          const float2 m = M[moff + i * D + k];
+          acc = zadd(acc, zmul(Z{m.x, m.y}, Bm[k * D + j]));
+        }
+        T[i * D + j] = acc;
+      }
+    for (int i = 0; i < D; ++i)  // B = T M^dag
+      for (int j = 0; j < D; ++j) {
+        Z acc{0, 0};
+        for (int k = 0; k < D; ++k) {
+          const float2 m = M[moff + j * D + k];
+          acc = zadd(acc, zmul(T[i * D + k], Z{m.x, -m.y}));
+        }
+        Bm[i * D + j] = acc;
+      }
+    double val = 0.0;
+    if (goff >= 0) {  // Re Tr(G B)
+      const double* G = gens + (size_t)goff * 2;
+      for (int i = 0; i < D; ++i)
+        for (int k = 0; k < D; ++k) {
+          const Z g{G[(i * D + k) * 2], G[(i * D + k) * 2 + 1]};
+          val += g.x * Bm[k * D + i].x - g.y * Bm[k * D + i].y;
+        }
+    }
+    out[(size_t)row * n_factors + f] = val;
+  }
+}
+
 __global__ void block_grads_kernel(const int32_t* __restrict__ blocks, int n_blocks,
                                    const int32_t* __restrict__ factors, const double* __restrict__ gens,
                                    const float2* __restrict__ mats, int n_mat, const double* __restrict__ a, int n_a,
@@ -744,53 +798,13 @@ __global__ void block_grads_kernel(const int32_t* __restrict__ blocks, int n_blo
   if (tid >= (int64_t)rows * n_blocks) return;
   const int row = (int)(tid / n_blocks), b = (int)(tid % n_blocks);
   const int fb = blocks[b * 4], fe = blocks[b * 4 + 1], D = blocks[b * 4 + 2], slot0 = blocks[b * 4 + 3];
-  const double* A = a + (size_t)row * n_a + slot0;
-  const float2* M = mats + (size_t)row * n_mat;
-  Z W[16], T[16];
-  for (int i = 0; i < D; ++i)
-    for (int j = 0; j < D; ++j) W[i * D + j] = {i == j ? 1.0 : 0.0, 0.0};
-  for (int f = fb; f < fe; ++f) {
-    const int moff = factors[f * 3], goff = factors[f * 3 + 1];
-    for (int i = 0; i < D; ++i)  // W <- M_f W
-      for (int j = 0; j < D; ++j) {
-        Z acc{0, 0};
-        for (int k = 0; k < D; ++k) {
-          const float2 m = M[moff + i * D + k];
-          acc = zadd(acc, zmul(Z{m.x, m.y}, W[k * D + j]));
-        }
-        T[i * D + j] = acc;
-      }
-    for (int i = 0; i < D * D; ++i) W[i] = T[i];
-    if (goff < 0) {
-      out[(size_t)row * n_factors + f] = 0.0;
-      continue;
-    }
-    const double* G = gens + (size_t)goff * 2;
-    for (int i = 0; i < D; ++i)  // T = G W
-      for (int j = 0; j < D; ++j) {
-        Z acc{0, 0};
-        for (int k = 0; k < D; ++k) acc = zadd(acc, zmul(Z{G[(i * D + k) * 2], G[(i * D + k) * 2 + 1]}, W[k * D + j]));
-        T[i * D + j] = acc;
-      }
-    // K[r][c] = sum_i conj(W[i][r]) T[i][c]; value = sum_j Re K[j][j] A_jj
-    //   + sum_{j<k} (Re K[k][j] * 2Re A_jk - Im K[k][j] * 2Im A_jk)
-    double val = 0.0;
-    int e = D;
-    for (int j = 0; j < D; ++j) {
-      for (int k = j; k < D; ++k) {
-        Z acc{0, 0};
-        for (int i = 0; i < D; ++i) acc = zadd(acc, zmul(Z{W[i * D + k].x, -W[i * D + k].y}, T[i * D + j]));
-        if (k == j) {
-          val += acc.x * A[j];
-        } else {
-          val += acc.x * A[e] - acc.y * A[e + 1];
-          e += 2;
-        }
-      }
-    }
-    out[(size_t)row * n_factors + f] = val;
-  }
+  if (D == 4)
+    block_grads_row<4>(fb, fe, slot0, row, factors, gens, mats, n_mat, a, n_a, out, n_factors);
+  else
+    block_grads_row<2>(fb, fe, slot0, row, factors, gens, mats, n_mat, a, n_a, out, n_factors);
 }
+
+}  // extern "C++"
 
 int qf_block_grads(const int32_t* blocks, int n_blocks, const int32_t* factors, int n_factors, const double* gens,
                    const float* mats, int n_mat, const double* a, int n_a, double* out, int rows, void* stream) {
