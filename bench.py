@@ -48,7 +48,7 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks / throttle reasons sampled during the timed region (NVML, else nvidia-smi)."""
 
     def __init__(self, index=0):
         self.index = index
@@ -56,7 +56,42 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
+    def _nvml_handle(self):
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            try:
+                pr = torch.cuda.get_device_properties(self.index)
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        except Exception:
+            return None, None
+
     def start(self):
+        nv, h = self._nvml_handle()
+        if h is not None:   # NVML: a sample every 5 ms (nvidia-smi takes ~100 ms per query)
+            def run_nvml():
+                get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                while not self._stop.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        r = get_r(h)
+                        flags = ["Active" if r & bit else "Not Active" for bit in (0x8, 0x40, 0x20, 0x4)]
+                        self.samples.append([str(sm), str(mx)] + flags)
+                    except Exception:
+                        pass
+                    self._stop.wait(0.005)
+
+            self._t = threading.Thread(target=run_nvml, daemon=True)
+            self._t.start()
+            return
+
         def run():
             q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
                  "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
