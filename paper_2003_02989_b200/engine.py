@@ -38,6 +38,19 @@ def _total_memory(device) -> int:
     return _TOTAL_MEM[idx]
 
 
+class UniformBatch(list):
+    """B rows of ONE circuit object (what ``ops.*`` build when a single circuit is passed):
+    binding skips the per-row identity scans (the parameter-shift path binds 2*K*B rows)."""
+
+    def __init__(self, circuit, rows: int):
+        super().__init__([circuit] * rows)
+        self.circuit = circuit
+
+
+def _uniform(circuits) -> bool:
+    return isinstance(circuits, UniformBatch)
+
+
 def _ptr(t) -> int:
     return 0 if t is None else t.data_ptr()
 
@@ -204,10 +217,11 @@ class Bound:
         self.from_state = from_state
         self.symbol_names = list(symbol_names)
         sym_index = {s: i for i, s in enumerate(self.symbol_names)}
-        self.circuits = list(circuits)
+        uniform = _uniform(circuits)
+        self.circuits = circuits if uniform else list(circuits)
         template = self.circuits[0]
         seen = set()
-        for c in self.circuits:
+        for c in ((template,) if uniform else self.circuits):
             if id(c) in seen:
                 continue
             seen.add(id(c))
@@ -246,7 +260,7 @@ class Bound:
                  and bool(obs.diag_ids) and not obs.generic_ids and (not want_grad or self.lam_diag)
                  and _jit.enabled(len(self.circuits), max(n, pl.N_MIN)))
         over = pl.batch_overrides(template, self.circuits, sym_index, pl.analyse(template, sym_index)) \
-            if len(self.circuits) > 1 else {}
+            if len(self.circuits) > 1 and not uniform else {}
         # block-fused adjoint (planner.build_ops(block=True)): plan-specialised kernels only
         block = (want_grad and os.environ.get("QF_BLOCK_ADJ", "1") not in ("0", "", "false")
                  and _jit.enabled(len(self.circuits), max(n, pl.N_MIN)))
@@ -256,13 +270,13 @@ class Bound:
         plan = self.plan
         self.frame = plan.fwd.frame
 
-        fixed_np, const_np = pl.concrete_tables(self.circuits, plan.infos)
+        fixed_np, const_np = pl.concrete_tables(self.circuits[:1] if uniform else self.circuits, plan.infos)
         self.fixed_rows, self.const_rows = fixed_np.shape[0], const_np.shape[0]
         self.fixed_t = torch.from_numpy(fixed_np.view(np.float64)).to(device)
         self.const_t = torch.from_numpy(const_np).to(device)
         if plan.adj is not None:
             infos_a = plan.extra["adj_infos"]
-            fa, ca = pl.concrete_tables(self.circuits, infos_a)
+            fa, ca = pl.concrete_tables(self.circuits[:1] if uniform else self.circuits, infos_a)
             self.fixed_a = torch.from_numpy(fa.view(np.float64)).to(device)
             self.const_a = torch.from_numpy(ca).to(device)
             self.fixed_a_rows, self.const_a_rows = fa.shape[0], ca.shape[0]
@@ -565,11 +579,14 @@ class Engine:
         dev = _require_cuda(device)
         symbol_names = tuple(s.name if hasattr(s, "name") else s for s in symbol_names)
         observables = list(observables)
-        key = (tuple(map(id, circuits)), symbol_names, tuple(map(id, observables)), bool(want_grad), str(dev),
+        uniform = _uniform(circuits)
+        ckey = ("uniform", id(circuits.circuit), len(circuits)) if uniform else tuple(map(id, circuits))
+        key = (ckey, symbol_names, tuple(map(id, observables)), bool(want_grad), str(dev),
                bool(from_state), bool(want_state), bool(norm_identity), pl.FUSION_ENABLED)
         with self._lock:
             hit = self._bound.get(key)
-        if hit is not None and all(a is b for a, b in zip(hit.circuits, circuits)):
+        if hit is not None and (hit.circuits[0] is circuits[0] if uniform else
+                                all(a is b for a, b in zip(hit.circuits, circuits))):
             return hit
         b = Bound(self, circuits, symbol_names, observables, want_grad, dev, from_state, want_state,
                   norm_identity)

@@ -21,7 +21,7 @@ import torch
 
 from . import gates as lib_gates
 from .circuit import Circuit
-from .engine import ENGINE
+from .engine import ENGINE, UniformBatch
 from .pauli import as_pauli_sum
 from .sampling import bits_from_indices, derive_seed, philox_key, sample_indices
 
@@ -36,12 +36,12 @@ def _prep(circuits, symbol_values, symbol_names):
         vals = vals.reshape(1, -1) if len(symbol_names) else vals.reshape(-1, 0)
     B = int(vals.shape[0])
     if not isinstance(circuits, (list, tuple)):
-        circuits = [circuits] * B
+        circuits = UniformBatch(circuits, B)
     if len(circuits) != B:
         raise ValueError(f"{len(circuits)} circuits for {B} parameter rows")
     if B and vals.shape[1] != len(symbol_names):
         raise ValueError(f"symbol_values has {vals.shape[1]} columns for {len(symbol_names)} symbol names")
-    return list(circuits), vals, B, on_dev
+    return (circuits if isinstance(circuits, UniformBatch) else list(circuits)), vals, B, on_dev
 
 
 def _to_dev(vals, dev):
@@ -120,32 +120,36 @@ def expectation_and_ps_gradient(circuits, symbol_names, symbol_values, operators
         structs[key] = (ec, base, [(col[syms_c[si]], w) for si, w in occ])
     K = len(names0 or [])
     if K:
-        order = [b for bs in groups.values() for b in bs]
-        rows = np.empty((B, 2 * K, K))
-        circ_rows = []
+        # shifted parameter rows [B, 2K, K] built on the device: row (b, 2k / 2k+1) is base[b]
+        # with pseudo-symbol k shifted by +/- pi/4
+        dev = _device()
+        base_all = np.empty((B, K))
         for key, bs in groups.items():
-            ec, base, _ = structs[key]
-            for i, b in enumerate(bs):
-                r = np.repeat(base[i][None, :], 2 * K, axis=0)
-                r[np.arange(0, 2 * K, 2), np.arange(K)] += gr.SHIFT
-                r[np.arange(1, 2 * K, 2), np.arange(K)] -= gr.SHIFT
-                rows[b] = r
-        allrows = rows.reshape(B * 2 * K, K).astype(np.float32)
-        allc = [structs[id(circuits[b])][0] for b in range(B) for _ in range(2 * K)]
-        if len(groups) == 1:
-            allc = allc[0]
+            base_all[bs] = structs[key][1]
+        rows = torch.as_tensor(base_all, dtype=torch.float64, device=dev)[:, None, :].repeat(1, 2 * K, 1)
+        kk = torch.arange(K, device=dev)
+        rows[:, 2 * kk, kk] += gr.SHIFT
+        rows[:, 2 * kk + 1, kk] -= gr.SHIFT
+        allrows = rows.reshape(B * 2 * K, K).to(torch.float32)
         n_eff = max(circuits[0].num_qubits, 10)
         per = max(1, chunk_amps >> n_eff)
-        f = np.empty((B * 2 * K, len(ops)))
+        f = torch.empty((B * 2 * K, len(ops)), dtype=torch.float64, device=dev)
         for s0 in range(0, allrows.shape[0], per):
-            cs = allc if len(groups) == 1 else allc[s0:s0 + per]
-            f[s0:s0 + per] = expectation(cs, names0, allrows[s0:s0 + per], ops)
-        f = (f.reshape(B, K, 2, len(ops)) * up[:, None, None, :]).sum(axis=3)
-        d = f[:, :, 0] - f[:, :, 1]                                     # [B, K]
+            s1 = min(s0 + per, allrows.shape[0])
+            if len(groups) == 1:
+                cs = structs[next(iter(groups))][0]
+            else:
+                cs = [structs[id(circuits[r // (2 * K)])][0] for r in range(s0, s1)]
+            f[s0:s1] = expectation(cs, names0, allrows[s0:s1], ops)
+        upd = torch.as_tensor(up, dtype=torch.float64, device=dev)
+        f = (f.reshape(B, K, 2, len(ops)) * upd[:, None, None, :]).sum(dim=3)
+        d = (f[:, :, 0] - f[:, :, 1]).cpu().numpy()                     # [B, K]
         for key, bs in groups.items():
-            for k, (si, w) in enumerate(structs[key][2]):
-                grad[bs, si] += w * d[bs, k]
-        del order
+            occ = structs[key][2]
+            si = np.array([o[0] for o in occ], dtype=np.int64)
+            w = np.array([o[1] for o in occ], dtype=np.float64)
+            ix = np.asarray(bs, dtype=np.int64)
+            np.add.at(grad, (ix[:, None], si[None, :]), w[None, :] * d[ix])
     if on_dev:
         dev = vals.device
         return torch.as_tensor(e0, device=dev), torch.as_tensor(grad, device=dev)
@@ -158,6 +162,12 @@ def state(circuits, symbol_names, symbol_values):
     bound = ENGINE.bind(circuits, symbol_names, [])
     out = bound.execute(_to_dev(vals, bound.device), want_state=True, want_expect=False)
     return _out(out["state"], on_dev)
+
+
+def _device():
+    from .engine import _require_cuda
+
+    return _require_cuda(None)
 
 
 def _row_seeds(seed, B):
