@@ -116,16 +116,27 @@ __global__ void build_dense_kernel(const QfBuildRecipe R, const float* theta, in
           G[i * 4 + j] = val;
         }
     }
-    // M = G @ M
+    // M = G @ M (the first factor is G itself; a one-qubit factor of a two-qubit op only
+    // mixes pairs of rows: two terms per entry instead of four)
     Z N[16];
-    for (int i = 0; i < D; ++i)
-      for (int j = 0; j < D; ++j) {
-        Z acc{0, 0};
-        for (int k = 0; k < D; ++k) acc = zadd(acc, zmul(G[i * 4 + k], M[k * 4 + j]));
-        N[i * 4 + j] = acc;
+    if (f == R.dense_fbeg[op]) {
+      for (int i = 0; i < 16; ++i) N[i] = G[i];
+    } else if (D == 4 && (emb == 2 || emb == 3)) {
+      const int bit = emb == 2 ? 2 : 1;
+      for (int i = 0; i < 4; ++i) {
+        const int i0 = i & ~bit, i1 = i | bit;
+        for (int j = 0; j < 4; ++j)
+          N[i * 4 + j] = zadd(zmul(G[i * 4 + i0], M[i0 * 4 + j]), zmul(G[i * 4 + i1], M[i1 * 4 + j]));
       }
-    for (int i = 0; i < D; ++i)
-      for (int j = 0; j < D; ++j) M[i * 4 + j] = N[i * 4 + j];
+    } else {
+      for (int i = 0; i < D; ++i)
+        for (int j = 0; j < D; ++j) {
+          Z acc{0, 0};
+          for (int k = 0; k < D; ++k) acc = zadd(acc, zmul(G[i * 4 + k], M[k * 4 + j]));
+          N[i * 4 + j] = acc;
+        }
+    }
+    for (int i = 0; i < 16; ++i) M[i] = N[i];
   }
   float2* out = mats + (size_t)row * n_mat + R.dense_mat[op];
   for (int i = 0; i < D; ++i)
@@ -536,8 +547,12 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
       for (int i = 0; i < D; ++i)
         for (int j = 0; j < D; ++j) {
           Z acc{0, 0};
-          for (int k = 0; k < D; ++k)  // forward: U P ; adjoint: P^dag U = P U (real Pauli products)
-            acc = zadd(acc, adjoint ? zmul(P[i * D + k], U[k * D + j]) : zmul(U[i * D + k], P[k * D + j]));
+          for (int k = 0; k < D; ++k) {  // forward: U P ; adjoint: P^dag U = P U (real Pauli products)
+            const Z p = adjoint ? P[i * D + k] : P[k * D + j];
+            if (p.x == 0.0) continue;    // P is a signed permutation: one term per entry
+            acc = zadd(acc, adjoint ? Z{p.x * U[k * D + j].x, p.x * U[k * D + j].y}
+                                    : Z{p.x * U[i * D + k].x, p.x * U[i * D + k].y});
+          }
           N[i * D + j] = acc;
         }
       for (int i = 0; i < D * D; ++i) M[off + i] = make_float2((float)N[i].x, (float)N[i].y);
