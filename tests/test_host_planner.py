@@ -173,3 +173,33 @@ def test_block_fused_adjoint_emulated_vs_oracle(n):
     theta = params[:1, :len(circuit_symbols(circ))].astype(np.float64)
     obs = PauliSum([PauliString(1.0, {n - 1: "Z"}), PauliString(0.3, {0: "Z", 1: "Z"})])
     _check_program(circ, obs, max(n, pl.N_MIN), theta, block=True)
+
+
+def test_block_mode_keeps_per_gate_programs_where_blocks_do_not_pay():
+    """build_ops(block=True): QAOA (single-symbol rotations, ZZ phase layers) is op-for-op the
+    per-gate adjoint program; a QCNN conv block becomes one two-qubit block of >= 3 symbolic
+    factors; one-qubit runs are split back to one op per gate."""
+    circ, cost = wl.qaoa_circuit(12, 3, wl.qaoa_graph(12))
+    si = {s: i for i, s in enumerate(circuit_symbols(circ))}
+    a = pl.build_ops(pl.analyse(circ, si), True, block=False)
+    b = pl.build_ops(pl.analyse(circ, si), True, block=True)
+    assert [(o.kind, o.qubits, o.factors, o.gates) for o in a] == [(o.kind, o.qubits, o.factors, o.gates) for o in b]
+    model = wl.qcnn_model(4)
+    si = {s: i for i, s in enumerate(circuit_symbols(model))}
+    infos = pl.analyse(model, si)
+    ops_b = pl.build_ops(infos, True, block=True)
+    blocks = [o for o in ops_b if o.symbolic and len(o.factors) > 1]
+    assert blocks and all(o.kind == pl.OP_DENSE2 for o in blocks)
+    assert all(sum(infos[g].symbolic for g in o.factors) >= pl.BLOCK_MIN_SYMBOLIC for o in blocks)
+    assert all(len(o.factors) == 1 for o in ops_b if o.kind == pl.OP_DENSE1)
+    # every gate appears exactly once
+    seen = sorted(g for o in ops_b for g in (o.factors or o.gates))
+    assert seen == list(range(len(infos)))
+
+
+def test_uniform_batch_is_a_list_of_one_circuit():
+    from paper_2003_02989_b200.engine import UniformBatch
+
+    c = wl.hea_circuit(4, 1)
+    u = UniformBatch(c, 5)
+    assert len(u) == 5 and all(x is c for x in u) and u.circuit is c and isinstance(u, list)
