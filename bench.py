@@ -312,10 +312,10 @@ def run_gpu(args, rank, world):
         pm = (_ptr(ckpt[1]), ckpt[1].shape[1]) if ckpt else (None, 0)
         nat.check(lib.qf_frame_walk_ckpt(_ptr(fw.t_events), fw.n_events, 0, B, _ptr(mats_f), fw.prog.n_mat,
                                          _ptr(angs_f), fw.prog.n_ang, _ptr(sc_f), fw.prog.n_slots, None, _ptr(fr),
-                                         pm[0], pm[1], s))
+                                         pm[0], pm[1], fw.n_stage, s))
         nat.check(lib.qf_frame_walk_ckpt(_ptr(ad.t_events), ad.n_events, 1, B, _ptr(mats_a), ad.prog.n_mat,
                                          _ptr(angs_a), ad.prog.n_ang, _ptr(sc_a), ad.prog.n_slots, _ptr(fr), None,
-                                         pm[0], pm[1], s))
+                                         pm[0], pm[1], ad.n_stage, s))
     part_f = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
     part_a = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
     hw = torch.ones((B, max(len(bound.hkeys), 1)), dtype=torch.float32, device=dev)

@@ -185,10 +185,12 @@ int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, fl
 
 /* qf_frame_walk for checkpointed adjoint sweeps: pass-boundary events record the stored
  * state's scale per forward pass into pass_m [rows, n_pass] (forward) or reload it from there
- * (adjoint, whose passes read psi from the forward's pass outputs). */
+ * (adjoint, whose passes read psi from the forward's pass outputs).  n_stage (0 = n_mat): the
+ * prefix of each row's slab the events touch, staged in shared memory (a block-fused adjoint's
+ * per-factor matrices follow it). */
 int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int rows, float* mats, int n_mat,
                        int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
-                       QfFrame* frame_out, double* pass_m, int n_pass, void* stream);
+                       QfFrame* frame_out, double* pass_m, int n_pass, int n_stage, void* stream);
 
 /* Block-fused adjoint (planner.build_program(block=True)): per (row, block) the gradient
  * value Tr(W_f^dag G_f W_f A) of every factor f of a fused dense block from the block's

@@ -79,7 +79,7 @@ def load(build_if_missing: bool = True):
     lib.qf_frame_walk.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, C.c_int, _p, C.c_int, _p, C.c_int, _p, _p,
                                   _p]
     lib.qf_frame_walk_ckpt.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, C.c_int, _p, C.c_int, _p, C.c_int, _p,
-                                       _p, _p, C.c_int, _p]
+                                       _p, _p, C.c_int, C.c_int, _p]
     lib.qf_block_grads.argtypes = [_p, C.c_int, _p, C.c_int, _p, _p, C.c_int, _p, C.c_int, _p, C.c_int, _p]
     lib.qf_pauli_expect.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _i64, _p, _p]
     lib.qf_pauli_apply.argtypes = [_p, _p, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _i64, _p]

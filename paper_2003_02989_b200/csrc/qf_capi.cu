@@ -581,20 +581,21 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
 __global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int adjoint, int rows,
                                   float2* mats, int n_mat, int32_t* angles, int n_ang, double* slot_scale,
                                   int n_slots, const QfFrame* frame_in, QfFrame* frame_out, double* pass_m,
-                                  int n_pass) {
+                                  int n_pass, int n_stage) {
+  // n_stage <= n_mat: the slab prefix the events touch (block factor matrices follow it)
   extern __shared__ __align__(16) unsigned char fw_smem[];
   float2* Ms = reinterpret_cast<float2*>(fw_smem);
-  int32_t* Es = reinterpret_cast<int32_t*>(Ms + n_mat);
+  int32_t* Es = reinterpret_cast<int32_t*>(Ms + n_stage);
   const int row = blockIdx.x;
   float2* M = mats + (size_t)row * n_mat;
-  for (int i = threadIdx.x; i < n_mat; i += blockDim.x) Ms[i] = M[i];
+  for (int i = threadIdx.x; i < n_stage; i += blockDim.x) Ms[i] = M[i];
   for (int i = threadIdx.x; i < n_ev * 8; i += blockDim.x) Es[i] = ev[i];
   __syncthreads();
   if (threadIdx.x == 0)
     frame_walk_row(Es, n_ev, adjoint, row, Ms, angles, n_ang, slot_scale, n_slots, frame_in, frame_out, pass_m,
                    n_pass);
   __syncthreads();
-  for (int i = threadIdx.x; i < n_mat; i += blockDim.x) M[i] = Ms[i];
+  for (int i = threadIdx.x; i < n_stage; i += blockDim.x) M[i] = Ms[i];
 }
 
 // Fallback for slabs too large for shared memory: one thread per row on global memory.
@@ -721,9 +722,10 @@ int qf_reduce_slots_scaled(const double* partials, int rows, int n_slots, int ti
 
 int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int rows, float* mats, int n_mat,
                        int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
-                       QfFrame* frame_out, double* pass_m, int n_pass, void* stream) {
+                       QfFrame* frame_out, double* pass_m, int n_pass, int n_stage, void* stream) {
   if (rows == 0) return 0;
-  const size_t smem = (size_t)n_mat * sizeof(float2) + (size_t)n_events * 8 * sizeof(int32_t);
+  if (n_stage <= 0 || n_stage > n_mat) n_stage = n_mat;
+  const size_t smem = (size_t)n_stage * sizeof(float2) + (size_t)n_events * 8 * sizeof(int32_t);
   if (smem <= 96 * 1024) {
     static bool configured = false;
     if (!configured) {
@@ -732,7 +734,7 @@ int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int row
     }
     frame_walk_kernel<<<rows, 128, smem, (cudaStream_t)stream>>>(
         events, n_events, adjoint, rows, reinterpret_cast<float2*>(mats), n_mat, angles, n_ang, slot_scale,
-        n_slots, frame_in, frame_out, pass_m, n_pass);
+        n_slots, frame_in, frame_out, pass_m, n_pass, n_stage);
     return check_launch("frame_walk_kernel");
   }
   const int T = 128;
@@ -835,7 +837,7 @@ int qf_frame_walk(const int32_t* events, int n_events, int adjoint, int rows, fl
                   int32_t* angles, int n_ang, double* slot_scale, int n_slots, const QfFrame* frame_in,
                   QfFrame* frame_out, void* stream) {
   return qf_frame_walk_ckpt(events, n_events, adjoint, rows, mats, n_mat, angles, n_ang, slot_scale, n_slots,
-                            frame_in, frame_out, nullptr, 0, stream);
+                            frame_in, frame_out, nullptr, 0, 0, stream);
 }
 
 int qf_pauli_expect(const float* psi, int n, int rows, int n_terms, const uint32_t* xmask, const uint32_t* zmask,

@@ -99,6 +99,10 @@ class DeviceProgram:
         ev = prog.frame_events if prog.frame_events is not None else np.zeros((0, pl.EV_INTS), np.int32)
         self.n_events = int(ev.shape[0])
         self.t_events = up(ev.reshape(-1), torch.int32)
+        # slab prefix the frame walk touches (block factor matrices are allocated after it)
+        span = [int(e[3]) + (16 if int(e[0]) in (pl.EV_ABS2, pl.EV_NP) else 4)
+                for e in ev if int(e[0]) in (pl.EV_NX, pl.EV_NY, pl.EV_ABS1, pl.EV_ABS2, pl.EV_NP)]
+        self.n_stage = min(max(span, default=1), max(prog.n_mat, 1))
         # block-fused adjoint: A slots reduced into consecutive columns, one range per block
         blk = prog.blocks if prog.blocks is not None else np.zeros((0, 4), np.int32)
         self.n_blocks = int(blk.shape[0])
@@ -376,7 +380,7 @@ class Bound:
             pm = (_ptr(ckpt[1]), ckpt[1].shape[1]) if ckpt else (None, 0)
             nat.check(lib.qf_frame_walk_ckpt(_ptr(fw.t_events), fw.n_events, 0, B, _ptr(mats), fw.prog.n_mat,
                                              _ptr(angs), fw.prog.n_ang, _ptr(scale), fw.prog.n_slots, None,
-                                             _ptr(frame_f), pm[0], pm[1], stream))
+                                             _ptr(frame_f), pm[0], pm[1], fw.n_stage, stream))
         else:
             frame_f = None
         partials = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
@@ -463,7 +467,7 @@ class Bound:
             pm = (_ptr(ckpt[1]), ckpt[1].shape[1]) if ckpt else (None, 0)
             nat.check(lib.qf_frame_walk_ckpt(_ptr(ad.t_events), ad.n_events, 1, B, _ptr(mats), ad.prog.n_mat,
                                              _ptr(angs), ad.prog.n_ang, _ptr(scale), ad.prog.n_slots, _ptr(frame_f),
-                                             None, pm[0], pm[1], stream))
+                                             None, pm[0], pm[1], ad.n_stage, stream))
         lam = torch.empty_like(psi)
         if not self.lam_diag:
             if self.hkeys:
