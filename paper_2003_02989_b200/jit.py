@@ -282,9 +282,10 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         w(f'extern "C" __global__ void __launch_bounds__({NT}, {minb_p}) {name}(const QfJitArgs a) {{')
         w("  extern __shared__ __align__(16) unsigned char smem_raw[];")
         w("  float2* sm = reinterpret_cast<float2*>(smem_raw);")
-        w(f"  float2* M = sm + {NA * TILE};")
-        w(f"  u64* MN = reinterpret_cast<u64*>(M + {mcnt});   // (-Im, Im) pairs of M")
-        w(f"  int* ANG = reinterpret_cast<int*>(MN + {mcnt});")
+        # staged matrices: one 16-byte entry {Re, Im, -Im, Im} per element, so a dense apply
+        # reads the broadcast real part and the (-Im, Im) pair with one LDS.128
+        w(f"  float4* MM = reinterpret_cast<float4*>(sm + {NA * TILE});")
+        w(f"  int* ANG = reinterpret_cast<int*>(MM + {mcnt});")
         w(f"  float* CO = reinterpret_cast<float*>(ANG + {acnt});")
         w(f"  float* GS = CO + {ccnt};")
         if ws_floats:
@@ -337,7 +338,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             # stage the row's matrices: as built for the forward sweep; conjugate-transposed
             # (U^dag) for general / X-like / real dense ops of the adjoint sweep
             w(f"  {{ const float2* __restrict__ src = a.mats + (size_t)row * a.n_mat + {mb};")
-            w(f"    for (int i = t; i < {mcnt}; i += {NT}) {{ const float2 x = src[i]; M[i] = x; MN[i] = pk_negpos(x.y); }}")
+            w(f"    for (int i = t; i < {mcnt}; i += {NT}) {{ const float2 x = src[i]; MM[i] = make_float4(x.x, x.y, -x.y, x.y); }}")
             if adj:
                 for op_ in pass_ops:
                     kd, cl_ = int(op_[0]), int(op_[9])
@@ -347,7 +348,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     off = int(op_[3]) - mb
                     w(f"    __syncthreads();")
                     w(f"    if (t < {D * D}) {{ const float2 x = src[{off} + (t % {D}) * {D} + t / {D}];"
-                      f" M[{off} + t] = make_float2(x.x, -x.y); MN[{off} + t] = pk_negpos(-x.y); }}")
+                      f" MM[{off} + t] = make_float4(x.x, -x.y, x.y, -x.y); }}")
             w("  }")
         if acnt:
             w(f"  for (int i = t; i < {acnt}; i += {NT}) ANG[i] = a.angles[(size_t)row * a.n_ang + {ab} + i];")
@@ -440,12 +441,12 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 if mo < 0:
                     w(f"  if ((gt0 >> {q}) & 1u) c = make_float2(0.f, 0.f);")
                 else:
-                    w(f"  c = cmul(c, ((gt0 >> {q}) & 1u) ? M[{mo - mb + 2}] : M[{mo - mb}]);")
+                    w(f"  c = cmul(c, ((gt0 >> {q}) & 1u) ? mm2(MM, {mo - mb + 2}) : mm2(MM, {mo - mb}));")
             w("  v0[0] = c;")
             for j in range(R):
                 mo = init_mat[int(st0[j])]
-                f0 = "make_float2(1.f, 0.f)" if mo < 0 else f"M[{mo - mb}]"
-                f1 = "make_float2(0.f, 0.f)" if mo < 0 else f"M[{mo - mb + 2}]"
+                f0 = "make_float2(1.f, 0.f)" if mo < 0 else f"mm2(MM, {mo - mb})"
+                f1 = "make_float2(0.f, 0.f)" if mo < 0 else f"mm2(MM, {mo - mb + 2})"
                 w(f"  {{ const float2 f0 = {f0}, f1 = {f1};")
                 for r in range(1 << j):
                     w(f"    v0[{r | (1 << j)}] = cmul(v0[{r}], f1); v0[{r}] = cmul(v0[{r}], f0);")
@@ -496,7 +497,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 if kind == pl.OP_DENSE1 and cls in (pl.CLS_NX, pl.CLS_NY):
                     # Pauli-frame normalised rotation: the build step wrote tau (adjoint-ready)
                     ax = 1 if cls == pl.CLS_NX else 2
-                    w(f"    {{ const float tau = M[{moff}].x;")
+                    w(f"    {{ const float tau = MM[{moff}].x;")
                     if adj and slot >= 0 and FUSED_GRAD:
                         g0 = int(op[8])
                         sc = float(gm[g0 + 4, 0])
@@ -514,11 +515,12 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     # adjoint: apply U^dag first, then the gradient slot -- G commutes with
                     # U = exp(-i v G), so Im<lam|G|psi> is the same on either side, and after
                     # the apply the Pauli frame on the op's qubits has been absorbed
-                    w(f"    {{ const float2 u00 = M[{moff}], u01 = M[{moff + 1}], u10 = M[{moff + 2}], u11 = M[{moff + 3}];")
+                    w(f"    {{ const float2 u00 = mm2(MM, {moff}), u01 = mm2(MM, {moff + 1}), u10 = mm2(MM, {moff + 2}),"
+                      f" u11 = mm2(MM, {moff + 3});")
                     if cls == pl.CLS_GENERAL:
                         if adj:
-                            w(f"      apply1m<{s0}, {NR}>(v1, M + {moff}, MN + {moff});")
-                        w(f"      apply1m<{s0}, {NR}>(v0, M + {moff}, MN + {moff});")
+                            w(f"      apply1m<{s0}, {NR}>(v1, MM + {moff});")
+                        w(f"      apply1m<{s0}, {NR}>(v0, MM + {moff});")
                     else:
                         if adj:
                             w(f"      apply1<{s0}, {NR}, {cls}>(v1, u00, u01, u10, u11);")
@@ -537,7 +539,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     w("    }")
                 elif kind == pl.OP_DENSE2 and cls == pl.CLS_NP:
                     code = int(op[12])
-                    w(f"    {{ const float tau = M[{moff}].x;")
+                    w(f"    {{ const float tau = MM[{moff}].x;")
                     if adj and slot >= 0:
                         g0 = int(op[8])
                         sc = float(gm[g0 + 16, 0])
@@ -548,8 +550,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 elif kind == pl.OP_DENSE2:
                     if adj:
                         w("    {")
-                        w(f"      apply2m<{s0}, {s1}, {NR}>(v0, M + {moff}, MN + {moff});"
-                          f" apply2m<{s0}, {s1}, {NR}>(v1, M + {moff}, MN + {moff});")
+                        w(f"      apply2m<{s0}, {s1}, {NR}>(v0, MM + {moff});"
+                          f" apply2m<{s0}, {s1}, {NR}>(v1, MM + {moff});")
                         if slot >= 0 and int(op[13]):
                             o.extend(_block_code(4, 1 << s0, 1 << s1, slot - slb, gs_store, "      ", NR))
                         elif slot >= 0:
@@ -560,7 +562,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                             w("      " + gs_store(slot - slb, f"grad2<{s0}, {s1}, {NR}>(v0, v1, g)"))
                         w("    }")
                     else:
-                        w(f"    apply2m<{s0}, {s1}, {NR}>(v0, M + {moff}, MN + {moff});")
+                        w(f"    apply2m<{s0}, {s1}, {NR}>(v0, MM + {moff});")
                 elif kind in (pl.OP_DIAG, pl.OP_OBS):
                     tb, te = int(op[4]), int(op[5])
                     groups: dict = {}

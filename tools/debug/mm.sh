@@ -1,0 +1,3 @@
+python -c "import __graft_entry__ as g; g.build()" >/dev/null 2>&1
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+timeout 900 python tools/configs_bench.py --steps 3
