@@ -247,6 +247,11 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         heavy = any(int(op_[0]) == pl.OP_DENSE2 or (int(op_[0]) == pl.OP_DENSE1 and int(op_[9]) == pl.CLS_GENERAL)
                     for op_ in pass_ops)
         minb_p = min(minb, max(1, 65536 // (NT * 128))) if (heavy and not env_minb) else minb
+        n_dense2 = sum(int(op_[0]) == pl.OP_DENSE2 for op_ in pass_ops)
+        if not adj and R == 5 and n_dense2 >= 4 and not env_minb:
+            # 32 amplitudes per thread plus 4x4 matrices spill at 128 registers: 168 (3 CTAs/SM)
+            # is faster (QCNN forward passes 21.9 -> 20.3 ms)
+            minb_p = min(minb_p, 3)
 
         flushes = [0]
 
