@@ -163,9 +163,10 @@ def _block_code(D: int, mhi: int, mlo: int, slot_rel: int, gs_store, indent: str
         e += 1
     for j in range(D):
         for k in range(j + 1, D):
-            for part in (1, 2):
-                lines.append(indent + gs_store(slot_rel + e, f"blk_entry<{NR}, {mhi}, {mlo}, {j}, {k}, {part}>(v0, v1)"))
-                e += 1
+            lines.append(indent + f"{{ const float2 bp = blk_pair<{NR}, {mhi}, {mlo}, {j}, {k}>(v0, v1);")
+            lines.append(indent + "  " + gs_store(slot_rel + e, "bp.x"))
+            lines.append(indent + "  " + gs_store(slot_rel + e + 1, "bp.y") + " }")
+            e += 2
     return lines
 
 
