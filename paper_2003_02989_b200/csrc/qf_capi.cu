@@ -584,15 +584,15 @@ __global__ void frame_walk_kernel(const int32_t* __restrict__ ev, int n_ev, int 
                                   int n_pass, int n_stage) {
   // n_stage <= n_mat: the slab prefix the events touch (block factor matrices follow it)
   extern __shared__ __align__(16) unsigned char fw_smem[];
+  // the event list is the same for every row: read through L1/L2 instead of a per-CTA copy,
+  // so the shared-memory footprint (and the rows resident per SM) is set by the slab alone
   float2* Ms = reinterpret_cast<float2*>(fw_smem);
-  int32_t* Es = reinterpret_cast<int32_t*>(Ms + n_stage);
   const int row = blockIdx.x;
   float2* M = mats + (size_t)row * n_mat;
   for (int i = threadIdx.x; i < n_stage; i += blockDim.x) Ms[i] = M[i];
-  for (int i = threadIdx.x; i < n_ev * 8; i += blockDim.x) Es[i] = ev[i];
   __syncthreads();
   if (threadIdx.x == 0)
-    frame_walk_row(Es, n_ev, adjoint, row, Ms, angles, n_ang, slot_scale, n_slots, frame_in, frame_out, pass_m,
+    frame_walk_row(ev, n_ev, adjoint, row, Ms, angles, n_ang, slot_scale, n_slots, frame_in, frame_out, pass_m,
                    n_pass);
   __syncthreads();
   for (int i = threadIdx.x; i < n_stage; i += blockDim.x) M[i] = Ms[i];
@@ -725,7 +725,7 @@ int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int row
                        QfFrame* frame_out, double* pass_m, int n_pass, int n_stage, void* stream) {
   if (rows == 0) return 0;
   if (n_stage <= 0 || n_stage > n_mat) n_stage = n_mat;
-  const size_t smem = (size_t)n_stage * sizeof(float2) + (size_t)n_events * 8 * sizeof(int32_t);
+  const size_t smem = (size_t)n_stage * sizeof(float2);
   if (smem <= 96 * 1024) {
     static bool configured = false;
     if (!configured) {
