@@ -203,3 +203,17 @@ def test_uniform_batch_is_a_list_of_one_circuit():
     c = wl.hea_circuit(4, 1)
     u = UniformBatch(c, 5)
     assert len(u) == 5 and all(x is c for x in u) and u.circuit is c and isinstance(u, list)
+
+
+@pytest.mark.parametrize("seed,n", [(0, 6), (1, 8), (2, 10), (3, 11)])
+def test_block_fused_adjoint_random_circuits_emulated(seed, n):
+    """Block-fused adjoint on random circuits (symbolic cnot_pow / Pauli-pair gates, fixed
+    dense gates and rotations mixed into two-qubit blocks), emulated against the oracle."""
+    rng = np.random.default_rng(500 + seed)
+    circ = random_circuit(rng, n, 120, n_sym=5, p2=0.5)
+    theta = rng.uniform(-2, 2, size=(2, len(circuit_symbols(circ))))
+    syms = circuit_symbols(circ)
+    si = {s: i for i, s in enumerate(syms)}
+    if not any(o.symbolic and len(o.factors) > 1 for o in pl.build_ops(pl.analyse(circ, si), True, block=True)):
+        pytest.skip("no block formed")
+    _check_program(circ, random_observable(rng, n, diag=True), max(n, pl.N_MIN), theta, block=True)
