@@ -94,6 +94,21 @@ __global__ void build_dense_kernel(const QfBuildRecipe R, const float* theta, in
       fd = (emb == 0 || emb == 1) ? 4 : 2;
     }
     (void)fd;
+    if (f != R.dense_fbeg[op] && (emb == 2 || emb == 3 || emb == 4)) {
+      // one-qubit factor: mix row pairs of M in place (no embedded 4x4 copy)
+      const int bit = emb == 2 ? 2 : 1;
+      const Z f00 = F[0], f01 = F[1], f10 = F[4], f11 = F[5];
+      for (int i0 = 0; i0 < D; ++i0) {
+        if (i0 & bit) continue;
+        const int i1 = i0 | bit;
+        for (int j = 0; j < D; ++j) {
+          const Z x = M[i0 * 4 + j], y = M[i1 * 4 + j];
+          M[i0 * 4 + j] = zadd(zmul(f00, x), zmul(f01, y));
+          M[i1 * 4 + j] = zadd(zmul(f10, x), zmul(f11, y));
+        }
+      }
+      continue;
+    }
     // embed F into the op's D-dim local space -> G
     Z G[16];
     if (emb == 4) {  // 1q op, 1q factor: F stored 2x2 at stride 4 or packed? -> packed 2x2 in [0..3]
@@ -116,18 +131,10 @@ __global__ void build_dense_kernel(const QfBuildRecipe R, const float* theta, in
           G[i * 4 + j] = val;
         }
     }
-    // M = G @ M (the first factor is G itself; a one-qubit factor of a two-qubit op only
-    // mixes pairs of rows: two terms per entry instead of four)
+    // M = G @ M (the first factor is G itself)
     Z N[16];
     if (f == R.dense_fbeg[op]) {
       for (int i = 0; i < 16; ++i) N[i] = G[i];
-    } else if (D == 4 && (emb == 2 || emb == 3)) {
-      const int bit = emb == 2 ? 2 : 1;
-      for (int i = 0; i < 4; ++i) {
-        const int i0 = i & ~bit, i1 = i | bit;
-        for (int j = 0; j < 4; ++j)
-          N[i * 4 + j] = zadd(zmul(G[i * 4 + i0], M[i0 * 4 + j]), zmul(G[i * 4 + i1], M[i1 * 4 + j]));
-      }
     } else {
       for (int i = 0; i < D; ++i)
         for (int j = 0; j < D; ++j) {
