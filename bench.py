@@ -28,7 +28,12 @@ import sys
 import threading
 import time
 
-import numpy as np
+# the CPU legs run one single-threaded reference process per host core: set the BLAS pool
+# size BEFORE numpy loads (OpenBLAS reads it once, at import), here and in every worker
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import numpy as np  # noqa: E402
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -139,75 +144,124 @@ def workload():
 # ---------------------------------------------------------------------------
 
 
-def _cpu_eval(args):
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    which, seed = args
+_JOBS = None
+
+
+def _row_jobs():
+    """The reference path for ONE row, as independent evaluations: the expectation plus the
+    2*sum K parameter-shift evaluations (ref gradients.py:241-326; oracle restatement
+    oracle/qcflow_port.parameter_shift_grad), each a fused simulate + exact expectation
+    (sim.py:139-150, :203-213).  Returns (n, observable, [op lists])."""
+    global _JOBS
+    if _JOBS is None:
+        from oracle import qcflow_port as orc
+        from paper_2003_02989_b200 import workloads as wl
+
+        circ, cost, syms = workload()
+        theta = wl.qaoa_params(BATCH, DEPTH)[0].astype(np.float64)
+        bind = dict(zip(syms, theta))
+        base = orc.resolved_ops(circ, bind)
+        jobs = [base]
+        for j, si, scale, v, terms in orc._occurrences(circ, bind, syms):
+            for k, t in enumerate(terms):
+                if scale * t.coefficient == 0.0:
+                    continue
+                for delta in (+orc.SHIFT, -orc.SHIFT):
+                    exp_ops = [orc._term_matrix(tt, v * tt.coefficient + (delta if kk == k else 0.0))
+                               for kk, tt in enumerate(terms)]
+                    jobs.append(base[:j] + exp_ops + base[j + 1:])
+        _JOBS = (N_QUBITS, cost, jobs)
+    return _JOBS
+
+
+def _cpu_eval(i):
+    """Evaluation i of the row (worker process, OpenBLAS single-threaded)."""
     from oracle import qcflow_port as orc
 
-    circ, cost, syms = workload()
-    from paper_2003_02989_b200 import workloads as wl
-
-    theta = wl.qaoa_params(BATCH, DEPTH)[seed % BATCH].astype(np.float64)
-    bind = dict(zip(syms, theta))
+    n, cost, jobs = _row_jobs()
     t0 = time.perf_counter()
-    if which == "expect":
-        amps = orc.simulate_amps(circ, bind)
-        orc.expectation(amps, cost, N_QUBITS)
-    else:  # one parameter-shift evaluation: a shifted fused simulation + expectation
-        ops = orc.resolved_ops(circ, bind)
-        z = np.zeros(2 ** N_QUBITS, dtype=np.complex128)
-        z[0] = 1.0
-        amps = orc.run_ops(z, ops, N_QUBITS, True)
-        orc.expectation(amps, cost, N_QUBITS)
+    z = np.zeros(2 ** n, dtype=np.complex128)
+    z[0] = 1.0
+    orc.expectation(orc.run_ops(z, jobs[i % len(jobs)], n, True), cost, n)
     return time.perf_counter() - t0
 
 
-def cpu_reference_rate(cores: int, rounds: int = 1):
-    """circuits/s of the reference path (expectation + parameter-shift gradient per row),
-    from a bounded sample: `rounds` x `cores` evaluations in parallel, extrapolated to the
-    2 * sum_occ K + 1 = 401 evaluations one 20q QAOA row costs."""
-    import multiprocessing as mp
+def _blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
 
-    circ, cost, syms = workload()
-    from oracle import qcflow_port as orc
+        return max((p.get("num_threads", 0) for p in threadpool_info() if p.get("internal_api") == "openblas"),
+                   default=None)
+    except Exception:
+        return None
 
-    n_evals = 1 + sum(2 * len([t for t in g.generator.terms if t.factors]) for g in circ.gates
-                      if g.exponent is not None and g.exponent.symbol is not None)
-    ctx = mp.get_context("fork")
-    t0 = time.perf_counter()
-    with ctx.Pool(cores) as pool:
-        per = pool.map(_cpu_eval, [("ps", i) for i in range(cores * rounds)])
-    wall = time.perf_counter() - t0
-    t_eval = float(np.mean(per))
-    rate = cores / (t_eval * n_evals)
-    return rate, dict(t_eval_s=t_eval, evals_per_circuit=n_evals, wall_s=wall,
-                      sample=f"{cores * rounds} fused 20q simulate+expectation evaluations on {cores} "
-                             f"processes, extrapolated to {n_evals} evaluations (1 expectation + PS) per circuit")
+
+class CpuReference:
+    """The reference's CPU path (oracle port) on every host core: a pool of single-threaded
+    processes, each step = one evaluation per core, walking through row 0's 401 evaluations
+    (1 expectation + 400 parameter-shift); at least one full row is always timed."""
+
+    def __init__(self, cores):
+        import multiprocessing as mp
+
+        self.cores = cores
+        self.ctx = mp.get_context("spawn")   # fresh interpreters: no CUDA / thread state inherited
+        self.pool = self.ctx.Pool(cores)
+        self.n_evals = len(_row_jobs()[2])
+        self.next = 0
+
+    def step(self):
+        ids = list(range(self.next, self.next + self.cores))
+        self.next += self.cores
+        return self.pool.map(_cpu_eval, ids, chunksize=1)
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_reference_rate(cores: int, steps: int = 1, warmup: int = 1):
+    """circuits/s of the reference path (expectation + parameter-shift gradient per row) on
+    ``cores`` processes; times max(steps, ceil(401 / cores)) steps so that at least one full
+    row's evaluations are covered."""
+    ref = CpuReference(cores)
+    try:
+        for _ in range(max(warmup, 0)):
+            ref.pool.map(_cpu_eval, [0] * cores, chunksize=1)    # imports + first-touch, untimed
+        n_steps = max(steps, -(-ref.n_evals // cores))
+        t0 = time.perf_counter()
+        per = []
+        for _ in range(n_steps):
+            per += ref.step()
+        wall = time.perf_counter() - t0
+    finally:
+        ref.close()
+    evals = n_steps * cores
+    rate = evals / wall / ref.n_evals            # rows (circuits) per second, all cores
+    return rate, dict(t_eval_s=float(np.mean(per)), evals_per_circuit=ref.n_evals, wall_s=wall,
+                      row_s=ref.n_evals * wall / evals, steps=n_steps, blas_threads=_blas_threads(),
+                      sample=f"{evals} evaluations ({evals / ref.n_evals:.2f} full 20q rows: 1 expectation + "
+                             f"{ref.n_evals - 1} parameter-shift evaluations each) on {cores} single-threaded "
+                             f"processes, {n_steps} steps of one evaluation per core")
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    rates = []
-    for _ in range(max(args.warmup, 0)):
-        pass  # warm-up is the pool start inside each step; no separate untimed work needed
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        r, info = cpu_reference_rate(cores)
-        rates.append(r)
-    wall = time.perf_counter() - t0
-    v = float(np.median(rates))
+    v, info = cpu_reference_rate(cores, args.steps, args.warmup)
     line = {
-        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH / v, "higher_is_better": True,
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": info["steps"],
+        "warmup": args.warmup, "ms_per_step": 1000.0 * info["wall_s"] / info["steps"], "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": "qaoa_maxcut_20q_p4_b256", "global_batch": BATCH, "n_qubits": N_QUBITS,
-                   "depth": DEPTH, "gradient": "parameter-shift (reference has no adjoint)"},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"]},
+                   "depth": DEPTH, "gradient": "parameter-shift (reference has no adjoint)",
+                   "step": "one 20q evaluation per host core"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"],
+                         "row_s": info["row_s"], "eval_s": info["t_eval_s"], "blas_threads": info["blas_threads"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": wall,
+        "wall_s": info["wall_s"],
     }
     print(json.dumps(line), flush=True)
 
@@ -249,7 +303,7 @@ def run_gpu(args, rank, world):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(args.backend or "nccl", device_id=dev)
     circ, cost, syms = workload()
     theta_np = wl.qaoa_params(BATCH * world, DEPTH)[rank * BATCH:(rank + 1) * BATCH]
     theta = torch.as_tensor(theta_np).to(dev)
@@ -367,11 +421,15 @@ def run_gpu(args, rank, world):
     tot_bytes = sum(fb) + sum(ab)
     tot_ms = times_f.sum() + times_a.sum()
     achieved = tot_bytes / (tot_ms / 1000.0) / 1e9
-    traffic = None
+    # DRAM traffic cannot be read in-run (no ncu inside a timed bench): it comes from the
+    # committed ncu capture of this same command, labelled with its source
+    traffic, traffic_src = None, None
     tr_path = os.path.join(ROOT, "profiles", "pass_kernel_traffic.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("bytes_per_step")
+            tr = json.load(open(tr_path))
+            if int(tr.get("algorithmic_bytes_per_step", -1)) == int(tot_bytes):
+                traffic, traffic_src = tr.get("bytes_per_step"), "from_profile: " + tr.get("source", tr_path)
         except Exception:
             traffic = None
 
@@ -393,15 +451,34 @@ def run_gpu(args, rank, world):
         e2e_ms = float(t.item())
     e2e = BATCH * world / (e2e_ms / 1000.0)
 
+    # ---- the same 256 rows with the reference's gradient rule (parameter shift) on the GPU:
+    # separates algorithm (adjoint vs PS) from hardware in the CPU comparison ----
+    ps = None
+    if not args.no_ps:
+        qops.expectation_and_ps_gradient(circ, syms, theta, [cost])     # warm-up (binding, JIT)
+        barrier()
+        e0.record(stream)
+        qops.expectation_and_ps_gradient(circ, syms, theta, [cost])
+        e1.record(stream)
+        barrier()
+        ps_ms = e0.elapsed_time(e1)
+        ps = {"value": BATCH / (ps_ms / 1000.0), "unit": UNIT, "ms_per_step": ps_ms,
+              "evaluations_per_circuit": 1 + 2 * sum(len([t for t in g.generator.terms if t.factors])
+                                                     for g in circ.gates
+                                                     if g.exponent is not None and g.exponent.symbol is not None),
+              "api": "ops.expectation_and_ps_gradient (device-resident rows, all shifted circuits batched)"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
-        r, info = cpu_reference_rate(cores)
-        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"]}
+        r, info = cpu_reference_rate(cores, 1, 1)
+        cpu = {"value": r, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"],
+               "row_s": info["row_s"], "eval_s": info["t_eval_s"], "blas_threads": info["blas_threads"]}
 
     if rank == 0:
-        # passes + 2 x (dense + angle build) + frame walks + 3 slot reductions (expectation,
-        # gradient, energy); cross-checked against the ncu launch list (profiles/)
+        # per step: passes + 2 builds (qf_build_ops: dense + angle kernels each) + 2 frame
+        # walks + 3 slot reductions (expectation, gradient, energy); no ATen kernels remain in
+        # the step (cross-checked against the ncu launch list under profiles/)
         launches = len(fb) + len(ab) + 4 + (2 if fw.frame else 0) + 3
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -417,6 +494,7 @@ def run_gpu(args, rank, world):
                     "d2h_bytes_per_step": int(BATCH * (1 + len(syms)) * 8)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "kernel": kname,
                          "algorithmic_bytes_per_step": tot_bytes, "kernel_ms_per_step": tot_ms,
                          "pass_ms": [round(x, 4) for x in list(times_f) + list(times_a)],
@@ -424,24 +502,177 @@ def run_gpu(args, rank, world):
                                       zip(list(fb) + list(ab), list(times_f) + list(times_a))]},
             "clocks": clocks,
             "cpu_baseline": cpu,
+            "gpu_parameter_shift": ps,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
-def main():
+def run_big32(args, rank, world):
+    """BASELINE cfg5: one 32-qubit brickwork circuit (depth 14), expectation of sum Z_i.  One
+    rank: the whole 32 GiB state on one GPU.  2^g ranks: the state sharded by g global qubits
+    (distributed.run_sharded), global/local swaps fused into the preceding tile pass over
+    NVLink peer memory (torch symmetric memory), NCCL all-to-all where that is unavailable."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2003_02989_b200 import distributed as D
+    from paper_2003_02989_b200 import workloads as wl
+    from paper_2003_02989_b200.engine import ENGINE
+
+    n = int(os.environ.get("QF_BIG_QUBITS", "32"))
+    g = world.bit_length() - 1
+    if world != 1 << g or g > 3:
+        raise SystemExit(f"big32 needs 1, 2, 4 or 8 ranks, got {world}")
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group(args.backend or "nccl", device_id=dev)
+    circ = wl.brickwork_circuit(n, 14, wl.SEED_BIG)
+    obs = wl.z_sum(n)
+    stream = torch.cuda.current_stream(dev)
+    if world == 1:
+        bound = ENGINE.bind([circ], [], [obs], device=dev)
+        theta = torch.zeros((1, 0), device=dev)
+
+        def step():
+            return bound.execute(theta)["expectations"]
+        swaps = 0
+        local_bytes = sum(pass_bytes(bound.plan.fwd.prog, 1))
+    else:
+        ex = D.NcclExchange(g)
+        plan = D.plan_segments(circ, g)
+
+        def step():
+            return D.run_sharded(circ, obs, g, ex, plan=plan)[0]
+        swaps = plan.swaps
+        local_bytes = None
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    e = float(res if not isinstance(res, torch.Tensor) else res.reshape(-1)[0])
+    if rank == 0:
+        peak, peak_kind = _peaks()
+        line = {"metric": f"circuits/sec ({n}q brickwork d14, expectation sum Z)", "value": 1000.0 / ms,
+                "unit": "circuits/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c64",
+                "data": "synthetic",
+                "config": {"workload": f"brickwork_{n}q_d14_seed{wl.SEED_BIG}", "global_qubits": g, "swaps": swaps,
+                           "parallelism": f"global-qubit shard x{world}" if world > 1 else "single GPU",
+                           "l2": f"inputs exceed L2 ({(8 << n) >> 30} GiB state)"},
+                "expectation": e, "clocks": clocks}
+        if local_bytes is not None:
+            achieved = local_bytes / (ms / 1000.0) / 1e9
+            line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                                "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                                "algorithmic_bytes_per_step": local_bytes,
+                                "note": "whole step (all pass kernels + reductions) over the pass algorithmic bytes"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_dry(args, rank, world):
+    """The multi-rank plumbing of the GPU arm without a GPU (CPU tests, gloo): each rank takes
+    its contiguous row shard of the headline batch, evaluates a 10-qubit stand-in of the
+    workload with the oracle (test infrastructure only), barriers, max-reduces its time and
+    rank 0 prints the JSON line."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import qcflow_port as orc
+    from paper_2003_02989_b200 import workloads as wl
+    from paper_2003_02989_b200.circuit import circuit_symbols
+    from paper_2003_02989_b200.parallel import shard_rows
+
+    if world > 1:
+        dist.init_process_group(args.backend or "gloo")
+    n, rows = 10, 8
+    circ, cost = wl.qaoa_circuit(n, 1, wl.qaoa_graph(n))
+    syms = circuit_symbols(circ)
+    theta = wl.qaoa_params(rows * world, 1)
+    a, b = shard_rows(rows * world, rank, world)
+    t0 = time.perf_counter()
+    vals = [orc.expectation(orc.simulate_amps(circ, dict(zip(syms, theta[r].astype(np.float64)))), cost, n)
+            for r in range(a, b)]
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64)
+    got = torch.tensor([float(b - a)], dtype=torch.float64)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(got, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "rows_evaluated": int(got.item()),
+                          "global_batch": rows * world, "value": float(got.item()) / float(dt.item()),
+                          "first_expectation": float(vals[0]) if vals else None}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch(argv, n: int) -> int:
+    """``--gpus N`` without a torchrun environment: start N ranks (one process per GPU) via
+    torch.distributed.run on 127.0.0.1 and pass their output through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="qaoa20", choices=["qaoa20", "big32"],
+                    help="qaoa20: BASELINE cfg2 (the headline); big32: cfg5, one 32-qubit circuit "
+                         "sharded by global qubits over the ranks")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    args = ap.parse_args()
+    ap.add_argument("--no-ps", action="store_true", help="skip the GPU parameter-shift leg")
+    ap.add_argument("--backend", default=None, help="process-group backend (default nccl; gloo for CPU tests)")
+    ap.add_argument("--dry-run", action="store_true", help="rank plumbing only, on CPU (tests)")
+    args = ap.parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(argv, args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if args.impl == "reference":
+    if args.dry_run:
+        run_dry(args, rank, world)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.workload == "big32":
+        run_big32(args, rank, world)
     else:
         run_gpu(args, rank, world)
 

@@ -165,6 +165,13 @@ int qf_reduce_slots_scaled(const double* partials, int rows, int n_slots, int ti
                            const int32_t* col_ptr, const int32_t* slot_list, int n_cols, double* out,
                            int accumulate, const double* slot_scale, void* stream);
 
+/* As qf_reduce_slots_scaled, plus col_offset[col] (nullable) added to every row's column:
+ * the identity terms of an observable (exact constants, qcflow/sim.py:203-213) folded into
+ * the reduction, so out needs no zero-fill or separate add. */
+int qf_reduce_slots_offset(const double* partials, int rows, int n_slots, int tiles,
+                           const int32_t* col_ptr, const int32_t* slot_list, int n_cols, double* out,
+                           int accumulate, const double* slot_scale, const double* col_offset, void* stream);
+
 /* Per-row Pauli frame of a normalised program: true state = sqrt(m) X^x Z^z stored state
  * (up to a global phase). */
 typedef struct QfFrame {
@@ -220,6 +227,13 @@ int qf_pauli_apply(const float* psi, float* lam, int n, int rows, int n_terms,
  * Philox starts at counter 1), out_idx [rows, shots] int64.  scratch: >= rows*(2^n/1024+2) doubles. */
 int qf_sample(const float* psi, int n, int rows, int shots, const uint64_t* keys,
               double* scratch, int64_t* out_idx, int32_t* near_boundary, void* stream);
+
+/* qf_sample with keys_per_row substreams per state row: keys [rows*keys_per_row*2],
+ * out_idx [rows, keys_per_row, shots], near_boundary [rows*keys_per_row].  One CDF per row
+ * serves every key: sampled_expectation draws each Pauli term k of a basis with
+ * substream(seed, k) from the same state (qcflow/sim.py:245-272). */
+int qf_sample_multi(const float* psi, int n, int rows, int keys_per_row, int shots, const uint64_t* keys,
+                    double* scratch, int64_t* out_idx, int32_t* near_boundary, void* stream);
 
 /* ---- plan-specialised kernels (jit.py generates CUDA source from the descriptors above) ---- */
 

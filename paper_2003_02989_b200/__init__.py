@@ -26,6 +26,7 @@ __version__ = "0.1.0"
 _LAZY = {
     "sim": ".sim", "gradients": ".gradients", "graph": ".graph", "ops": ".ops", "engine": ".engine",
     "planner": ".planner", "gates": ".gates", "workloads": ".workloads", "install": ".install",
+    "cli": ".cli",
 }
 _LAZY_ATTRS = {
     "simulate": "sim", "expectation": "sim", "batch_execute": "sim", "sample": "sim",

@@ -39,10 +39,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         flags += ["-Xptxas", "-v"]
     nvcc = nvcc_path()
-    for src in SOURCES:
+
+    def compile_one(src):
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
         cmd = [nvcc, *flags, "-c", os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:   # the translation units compile in parallel
+        results = list(ex.map(compile_one, SOURCES))
+    for src, obj, r in results:
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         if verbose:

@@ -179,7 +179,8 @@ __global__ void build_angle_kernel(const QfBuildRecipe R, const float* theta, in
 
 __global__ void reduce_slots_kernel(const double* __restrict__ partials, int rows, int n_slots, int tiles,
                                     const int32_t* col_ptr, const int32_t* slot_list, int n_cols,
-                                    double* out, int accumulate, const double* __restrict__ slot_scale) {
+                                    double* out, int accumulate, const double* __restrict__ slot_scale,
+                                    const double* __restrict__ col_offset) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= rows * n_cols) return;
@@ -192,6 +193,7 @@ __global__ void reduce_slots_kernel(const double* __restrict__ partials, int row
     part = warp_sum_d(part);
     acc += slot_scale ? part * slot_scale[(size_t)row * n_slots + slot_list[s]] : part;
   }
+  if (col_offset) acc += col_offset[col];
   if (lane == 0) out[(size_t)row * n_cols + col] = accumulate ? out[(size_t)row * n_cols + col] + acc : acc;
 }
 
@@ -348,17 +350,20 @@ __global__ void row_scan_kernel(const double* chunk_tot, int64_t nchunk, double*
   if (nchunk == 0 && t == 0) out[0] = 0.0;
 }
 
-__global__ void draw_kernel(const float2* __restrict__ psi, int n, int rows, int shots, const uint64_t* keys,
-                            const double* prefix, int64_t* out, int32_t* near) {
+// One warp per (row, key, shot): kper keys per state row (substream(seed, k) for every
+// term k of a sampled expectation draws from one CDF), output [rows, kper, shots].
+__global__ void draw_kernel(const float2* __restrict__ psi, int n, int rows, int kper, int shots,
+                            const uint64_t* keys, const double* prefix, int64_t* out, int32_t* near) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (warp >= (int64_t)rows * shots) return;
-  const int row = (int)(warp / shots);
+  if (warp >= (int64_t)rows * kper * shots) return;
+  const int krow = (int)(warp / shots);
+  const int row = krow / kper;
   const int64_t s = warp % shots;
   const int64_t nchunk = ((int64_t)1 << n) / kChunk;
   const double* pre = prefix + row * (nchunk + 1);
   const double total = pre[nchunk];
-  const double u = philox_uniform(keys[2 * row], keys[2 * row + 1], (uint64_t)s);
+  const double u = philox_uniform(keys[2 * krow], keys[2 * krow + 1], (uint64_t)s);
   const double target = u * total;
   // largest chunk c with pre[c] <= target  (c < nchunk)
   int64_t lo = 0, hi = nchunk - 1;
@@ -395,9 +400,9 @@ __global__ void draw_kernel(const float2* __restrict__ psi, int n, int rows, int
     before = after = base + __shfl_sync(0xffffffffu, incl, 31);
   }
   if (lane == 0) {
-    out[(int64_t)row * shots + s] = idx;
+    out[(int64_t)krow * shots + s] = idx;
     const double tol = 1e-12 * total;
-    if (near && (fabs(after - target) < tol || fabs(target - before) < tol)) atomicAdd(near + row, 1);
+    if (near && (fabs(after - target) < tol || fabs(target - before) < tol)) atomicAdd(near + krow, 1);
   }
 }
 
@@ -712,7 +717,7 @@ int qf_reduce_slots(const double* partials, int rows, int n_slots, int tiles, co
   const int64_t warps = (int64_t)rows * n_cols;
   const int T = 256;
   reduce_slots_kernel<<<(unsigned)((warps * 32 + T - 1) / T), T, 0, (cudaStream_t)stream>>>(
-      partials, rows, n_slots, tiles, col_ptr, slot_list, n_cols, out, accumulate, nullptr);
+      partials, rows, n_slots, tiles, col_ptr, slot_list, n_cols, out, accumulate, nullptr, nullptr);
   return check_launch("reduce_slots_kernel");
 }
 
@@ -723,7 +728,18 @@ int qf_reduce_slots_scaled(const double* partials, int rows, int n_slots, int ti
   const int64_t warps = (int64_t)rows * n_cols;
   const int T = 256;
   reduce_slots_kernel<<<(unsigned)((warps * 32 + T - 1) / T), T, 0, (cudaStream_t)stream>>>(
-      partials, rows, n_slots, tiles, col_ptr, slot_list, n_cols, out, accumulate, slot_scale);
+      partials, rows, n_slots, tiles, col_ptr, slot_list, n_cols, out, accumulate, slot_scale, nullptr);
+  return check_launch("reduce_slots_kernel");
+}
+
+int qf_reduce_slots_offset(const double* partials, int rows, int n_slots, int tiles, const int32_t* col_ptr,
+                           const int32_t* slot_list, int n_cols, double* out, int accumulate,
+                           const double* slot_scale, const double* col_offset, void* stream) {
+  if (rows == 0 || n_cols == 0) return 0;
+  const int64_t warps = (int64_t)rows * n_cols;
+  const int T = 256;
+  reduce_slots_kernel<<<(unsigned)((warps * 32 + T - 1) / T), T, 0, (cudaStream_t)stream>>>(
+      partials, rows, n_slots, tiles, col_ptr, slot_list, n_cols, out, accumulate, slot_scale, col_offset);
   return check_launch("reduce_slots_kernel");
 }
 
@@ -734,11 +750,8 @@ int qf_frame_walk_ckpt(const int32_t* events, int n_events, int adjoint, int row
   if (n_stage <= 0 || n_stage > n_mat) n_stage = n_mat;
   const size_t smem = (size_t)n_stage * sizeof(float2);
   if (smem <= 96 * 1024) {
-    static bool configured = false;
-    if (!configured) {
-      cudaFuncSetAttribute(frame_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      configured = true;
-    }
+    // per device context (and cheap): set on every call rather than behind a process-wide flag
+    cudaFuncSetAttribute(frame_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
     frame_walk_kernel<<<rows, 128, smem, (cudaStream_t)stream>>>(
         events, n_events, adjoint, rows, reinterpret_cast<float2*>(mats), n_mat, angles, n_ang, slot_scale,
         n_slots, frame_in, frame_out, pass_m, n_pass, n_stage);
@@ -872,9 +885,9 @@ int qf_pauli_apply(const float* psi, float* lam, int n, int rows, int n_terms, c
   return check_launch("pauli_apply_kernel");
 }
 
-int qf_sample(const float* psi, int n, int rows, int shots, const uint64_t* keys, double* scratch, int64_t* out_idx,
-              int32_t* near_boundary, void* stream) {
-  if (rows == 0 || shots == 0) return 0;
+int qf_sample_multi(const float* psi, int n, int rows, int keys_per_row, int shots, const uint64_t* keys,
+                    double* scratch, int64_t* out_idx, int32_t* near_boundary, void* stream) {
+  if (rows == 0 || shots == 0 || keys_per_row == 0) return 0;
   if (n < 10 || n > 32) {
     set_error("qf_sample: n=%d outside [10, 32] (callers pad small registers)", n);
     return 2;
@@ -889,10 +902,15 @@ int qf_sample(const float* psi, int n, int rows, int shots, const uint64_t* keys
   if (check_launch("chunk_sum_kernel")) return 1;
   row_scan_kernel<<<rows, 1024, 0, s>>>(chunk_tot, nchunk, prefix);
   if (check_launch("row_scan_kernel")) return 1;
-  const int64_t dw = (int64_t)rows * shots;
-  draw_kernel<<<(unsigned)((dw * 32 + 255) / 256), 256, 0, s>>>(p, n, rows, shots, keys, prefix, out_idx,
-                                                               near_boundary);
+  const int64_t dw = (int64_t)rows * keys_per_row * shots;
+  draw_kernel<<<(unsigned)((dw * 32 + 255) / 256), 256, 0, s>>>(p, n, rows, keys_per_row, shots, keys, prefix,
+                                                               out_idx, near_boundary);
   return check_launch("draw_kernel");
+}
+
+int qf_sample(const float* psi, int n, int rows, int shots, const uint64_t* keys, double* scratch, int64_t* out_idx,
+              int32_t* near_boundary, void* stream) {
+  return qf_sample_multi(psi, n, rows, 1, shots, keys, scratch, out_idx, near_boundary, stream);
 }
 
 }  // extern "C"

@@ -533,11 +533,8 @@ static int launch_pass(const PassArgs& a, const QfPass& hp, cudaStream_t stream)
                 (size_t)(hp.op_end - hp.op_begin) * sizeof(QfOp) + (size_t)(hp.slot_end - hp.slot_begin) * 8 * (NT / 32) +
                 (size_t)(hp.mat_end - hp.mat_begin) * sizeof(float2) + terms * 8 + (ADJ ? terms * 4 : 0) +
                 (size_t)(hp.grp_end - hp.grp_begin) * 4;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(pass_kernel<L, R, ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
-  }
+  // the attribute is per device context: set it on every launch (cheap) instead of once per process
+  cudaFuncSetAttribute(pass_kernel<L, R, ADJ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (smem > 200 * 1024) {
     set_error("pass %d needs %zu bytes of shared memory", a.pass, smem);
     return 3;

@@ -332,7 +332,11 @@ class LoopbackExchange:
 
 class NcclExchange:
     """One process per GPU: rank r owns shard r; swaps are one all_to_all_single
-    (torch.distributed, NCCL over NVLink on a B200 box; gloo on CPU in the tests)."""
+    (torch.distributed, NCCL over NVLink on a B200 box; gloo on CPU in the tests), or -- when
+    torch symmetric memory is available -- a store straight into the peers' shards by the
+    preceding tile pass (NVLink peer pointers).  The state lives in one of two symmetric
+    buffers, rendezvoused ONCE per shape: a fused swap writes into the peers' other buffer,
+    which becomes their state (ping-pong), so no swap re-allocates or re-rendezvouses."""
 
     def __init__(self, g: int, group=None):
         import torch.distributed as dist
@@ -345,7 +349,42 @@ class NcclExchange:
         self.g = g
         self.ranks = [dist.get_rank(group)]
         self._spare = None
-        self._symm = None
+        self._symm = None          # [(buffer, handle, peer-pointer tensor)] x 2, or False
+        self._hdl = None
+
+    def _symm_buffers(self, shape, dtype, device):
+        if self._symm is False:
+            return None
+        if self._symm is not None and self._symm[0][0].shape == shape:
+            return self._symm
+        try:
+            import torch
+            import torch.distributed._symmetric_memory as symm
+
+            grp = self.dist.group.WORLD if self.group is None else self.group
+            bufs = []
+            for _ in range(2):
+                buf = symm.empty(shape, dtype=dtype, device=device)
+                hdl = symm.rendezvous(buf, grp)
+                ptrs = torch.tensor([int(p) for p in hdl.buffer_ptrs], dtype=torch.int64, device=device)
+                bufs.append((buf, hdl, ptrs))
+            self._symm = bufs
+        except Exception:
+            self._symm = False
+            return None
+        return self._symm
+
+    def alloc_state(self, rows: int, dim: int, executor):
+        """This rank's initial shard, in symmetric memory when available (else None)."""
+        if not getattr(executor, "is_cuda", False):
+            return None
+        torch = executor.torch
+        bufs = self._symm_buffers((rows, dim), torch.complex64, executor.device)
+        if bufs is None:
+            return None
+        psi = bufs[0][0]
+        psi.zero_()
+        return psi
 
     def swap(self, psi, n_loc: int):
         if self._spare is None or self._spare.shape != psi.shape:
@@ -360,28 +399,23 @@ class NcclExchange:
         return x
 
     def remote_targets(self, psi):
-        """Fused swaps need every rank's receive shard mapped into this process (NVLink peer
-        memory): torch symmetric memory when available, else None (plain all-to-all)."""
-        try:
-            import torch
-            import torch.distributed._symmetric_memory as symm
-        except Exception:
+        """(peer pointers of every rank's receive shard, this rank, receive tensor) when psi is
+        one of the symmetric buffers, else None (plain all-to-all)."""
+        bufs = self._symm if self._symm else None
+        if not bufs:
             return None
-        try:
-            if self._symm is None or self._symm[0].shape != psi.shape:
-                buf = symm.empty(psi.shape, dtype=psi.dtype, device=psi.device)
-                hdl = symm.rendezvous(buf, self.dist.group.WORLD if self.group is None else self.group)
-                ptrs = torch.tensor([int(p) for p in hdl.buffer_ptrs], dtype=torch.int64, device=psi.device)
-                self._symm = (buf, hdl, ptrs)
-        except Exception:
+        ptr = psi.data_ptr()
+        if ptr == bufs[0][0].data_ptr():
+            buf, hdl, ptrs = bufs[1]
+        elif ptr == bufs[1][0].data_ptr():
+            buf, hdl, ptrs = bufs[0]
+        else:
             return None
-        buf, hdl, ptrs = self._symm
-        self._symm_hdl = hdl
+        self._hdl = hdl
         return ptrs, self.ranks[0], buf
 
     def remote_done(self):
-        self._symm_hdl.barrier()       # every rank's stores have landed before anyone reads
-        self._symm = None              # the received shard is now this rank's state
+        self._hdl.barrier()        # stream-ordered: every rank's stores have landed before anyone reads
 
 
 def _flat(t):
@@ -416,6 +450,7 @@ class EngineExecutor:
 
         self.torch = torch
         self.device = _require_cuda(device)
+        self.is_cuda = True
 
     def zeros(self, rows, dim):
         return self.torch.zeros((rows, dim), dtype=self.torch.complex64, device=self.device)
@@ -487,7 +522,10 @@ def run_sharded(circuit, observable, g: int, exchange, executor=None, symbol_nam
     vals = np.zeros((len(ranks), len(names)), dtype=np.float32)
     if values is not None:
         vals[:] = np.asarray(values, dtype=np.float32).reshape(1, -1)
-    psi = executor.zeros(len(ranks), 1 << n_loc)
+    alloc = getattr(exchange, "alloc_state", None)
+    psi = alloc(len(ranks), 1 << n_loc, executor) if alloc is not None else None
+    if psi is None:
+        psi = executor.zeros(len(ranks), 1 << n_loc)
     for i, r in enumerate(ranks):
         if r == 0:
             psi[i, 0] = 1.0

@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+from collections import OrderedDict
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -230,7 +231,7 @@ class Bound:
                 continue
             seen.add(id(c))
             if c.num_qubits != template.num_qubits:
-                raise ValueError("all circuits of a batch must have the same register size")
+                raise pl.TopologyMismatch("all circuits of a batch must have the same register size")
             for s in circuit_symbols(c):
                 if s not in sym_index:
                     raise KeyError(f"missing binding for symbol '{s}'")
@@ -255,6 +256,10 @@ class Bound:
                 for k, c in uniq[kk]:
                     M[k, j] += c
             self.hmix = torch.from_numpy(M).to(device)
+            # weights of the default upstream (all ones): H_b = sum_k obs_k for every row
+            self.hw_ones = torch.from_numpy(np.ascontiguousarray(
+                np.broadcast_to(M.sum(axis=0, keepdims=True), (len(self.circuits), M.shape[1])))).to(
+                device=device, dtype=torch.float32)
             self.lam_diag = bool(self.hkeys) and all(all(p == "Z" for _, p in kk) for kk in self.hkeys)
         # Pauli-frame normalisation (planner.build_program): only where every output is a
         # diagonal observable / adjoint gradient and the plan-specialised kernels run
@@ -398,11 +403,13 @@ class Bound:
                                         stream))
         out: dict = {}
         if self.n_obs and want_expect:
-            expv = torch.zeros((B, self.n_obs), dtype=torch.float64, device=dev)
-            if self.obs.diag_ids:
-                ptr, lst = self.obs_csr
-                nat.check(lib.qf_reduce_slots_scaled(_ptr(partials), B, fw.prog.n_slots, fw.tiles, _ptr(ptr),
-                                                     _ptr(lst), self.n_obs, _ptr(expv), 0, _ptr(scale), stream))
+            # the diagonal reduction writes every column (empty columns get 0) plus the identity
+            # constants: no zero-fill, no separate add
+            expv = torch.empty((B, self.n_obs), dtype=torch.float64, device=dev)
+            ptr, lst = self.obs_csr
+            nat.check(lib.qf_reduce_slots_offset(_ptr(partials), B, fw.prog.n_slots, fw.tiles, _ptr(ptr),
+                                                 _ptr(lst), self.n_obs, _ptr(expv), 0, _ptr(scale),
+                                                 _ptr(self.ident), stream))
             if self.gen_T:
                 xm, zm, ny, cf = self.gen_arrays
                 chunks = ((1 << n_eff) + 2047) // 2048
@@ -412,7 +419,6 @@ class Bound:
                 ptr, lst = self.gen_csr
                 nat.check(lib.qf_reduce_slots(_ptr(part), B, self.gen_T, chunks, _ptr(ptr), _ptr(lst), self.n_obs,
                                               _ptr(expv), 1, stream))
-            expv += self.ident
             out["expectations"] = expv
         if want_state:
             st = psi[:, : (1 << plan.n)]
@@ -448,14 +454,14 @@ class Bound:
         ad = plan.adj
         n_eff = plan.n_eff
         if upstream is None:
-            up = torch.ones((B, max(self.n_obs, 1)), dtype=torch.float64, device=dev)
+            hw_t = self.hw_ones   # precomputed at bind time: no per-step ATen work
         else:
             up = torch.as_tensor(upstream, dtype=torch.float64).to(dev).reshape(B, -1)
             if up.shape[1] != self.n_obs:
                 raise ValueError(f"upstream shape {tuple(up.shape)} != ({B}, {self.n_obs})")
-        # elementwise product + fixed-order sum: bit-identical across calls and threads (a
-        # cuBLAS GEMM may pick different reduction orders)
-        hw_t = (up[:, :, None] * self.hmix[None, :, :]).sum(dim=1).to(torch.float32).contiguous()
+            # elementwise product + fixed-order sum: bit-identical across calls and threads (a
+            # cuBLAS GEMM may pick different reduction orders)
+            hw_t = (up[:, :, None] * self.hmix[None, :, :]).sum(dim=1).to(torch.float32).contiguous()
         mats = torch.empty((B, max(ad.prog.n_mat, 1)), dtype=torch.complex64, device=dev)
         angs = torch.empty((B, max(ad.prog.n_ang, 1)), dtype=torch.int32, device=dev)
         rec = ad.recipe(self.fixed_a, self.fixed_a_rows, self.const_a, self.const_a_rows)
@@ -491,7 +497,9 @@ class Bound:
             nat.check(lib.qf_adjoint_passes(C.byref(struct), 0, len(ad.prog.passes), _ptr(psi), _ptr(lam), n_eff,
                                             B, _ptr(mats), _ptr(angs), _ptr(hw_t), _ptr(partials), ad.tiles,
                                             stream))
-        grad = torch.zeros((B, max(self.S, 1)), dtype=torch.float64, device=dev)
+        # every column is written by the first reduction (S > 0)
+        grad = torch.empty((B, self.S), dtype=torch.float64, device=dev) if self.S else \
+            torch.zeros((B, 1), dtype=torch.float64, device=dev)
         if self.S:
             ptr, lst = self.grad_csr
             nat.check(lib.qf_reduce_slots_scaled(_ptr(partials), B, ad.prog.n_slots, ad.tiles, _ptr(ptr), _ptr(lst),
@@ -517,11 +525,19 @@ class Bound:
         out["grad"] = grad[:, : self.S]
 
 
+def _obs_key(o) -> tuple:
+    """Content key of an observable (terms and coefficients): callers that pass a fresh
+    PauliString / reference PauliSum object per call still hit the binding cache."""
+    s = as_pauli_sum(o)
+    return tuple((tuple(sorted(t.factors.items())), float(t.coefficient)) for t in s.terms)
+
+
 class Engine:
-    def __init__(self, max_bound: int = 64):
-        self._plans: dict = {}
-        self._bound: dict = {}
+    def __init__(self, max_bound: int = 64, max_plans: int = 256):
+        self._plans: OrderedDict = OrderedDict()
+        self._bound: OrderedDict = OrderedDict()
         self._max_bound = max_bound
+        self._max_plans = max_plans
         self._lock = threading.Lock()
 
     def plan(self, template, symbol_index, obs: ObsInfo, adjoint: bool, lam_diag: bool, hkeys, device,
@@ -532,6 +548,8 @@ class Engine:
                tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block)
         with self._lock:
             hit = self._plans.get(key)
+            if hit is not None:
+                self._plans.move_to_end(key)
         if hit is not None:
             return hit
         n = template.num_qubits
@@ -576,6 +594,8 @@ class Engine:
             plan.extra["adj_infos"] = infos_a
         with self._lock:
             self._plans[key] = plan
+            while len(self._plans) > self._max_plans:   # LRU: device tables + NVRTC modules go with it
+                self._plans.popitem(last=False)
         return plan
 
     def bind(self, circuits, symbol_names, observables=(), *, want_grad=False, device=None,
@@ -585,10 +605,12 @@ class Engine:
         observables = list(observables)
         uniform = _uniform(circuits)
         ckey = ("uniform", id(circuits.circuit), len(circuits)) if uniform else tuple(map(id, circuits))
-        key = (ckey, symbol_names, tuple(map(id, observables)), bool(want_grad), str(dev),
+        key = (ckey, symbol_names, tuple(_obs_key(o) for o in observables), bool(want_grad), str(dev),
                bool(from_state), bool(want_state), bool(norm_identity), pl.FUSION_ENABLED)
         with self._lock:
             hit = self._bound.get(key)
+            if hit is not None:
+                self._bound.move_to_end(key)
         if hit is not None and (hit.circuits[0] is circuits[0] if uniform else
                                 all(a is b for a, b in zip(hit.circuits, circuits))):
             return hit
@@ -597,7 +619,7 @@ class Engine:
         b._keepalive = observables
         with self._lock:
             if len(self._bound) >= self._max_bound:
-                self._bound.pop(next(iter(self._bound)))
+                self._bound.popitem(last=False)
             self._bound[key] = b
         return b
 

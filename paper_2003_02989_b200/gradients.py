@@ -336,11 +336,60 @@ class FiniteDifference:
 # ---------------------------------------------------------------------------
 
 
+def _stochastic_walk(occs, cost, cmass, ctot, omass, otot, cfg):
+    """The reference's sampling walk (ref gradients.py:263-322), consuming substream(seed, i)
+    in exactly its order, WITHOUT evaluating anything: returns the evaluation list
+    [(i, occ index, term k, cost term m or -1, weight, counter)] (each entry = the f+ / f-
+    pair of keys (i, 0, counter) / (i, 1, counter)) and the degenerate flag."""
+    evals = []
+    degenerate = False
+    for i in range(cfg.num_samples):
+        rng = np.random.Generator(np.random.Philox(np.random.SeedSequence(cfg.seed, spawn_key=(i,))))
+        counter = 0
+        if cfg.sample_coordinates:
+            if otot == 0.0:
+                degenerate, chosen = True, []
+            else:
+                pr = omass / otot
+                pick = int(rng.choice(len(occs), p=pr))
+                chosen = [(pick, 1.0 / pr[pick])]
+        else:
+            chosen = [(o, 1.0) for o in range(len(occs))]
+        for oi, cw in chosen:
+            occ = occs[oi]
+            terms = occ[4]
+            btot = sum(abs(t.coefficient) for t in terms)
+            if cfg.sample_generator_terms:
+                if btot == 0.0:
+                    degenerate = True
+                    continue
+                k = int(rng.choice(len(terms), p=np.array([abs(t.coefficient) for t in terms]) / btot))
+                pairs = [(k, occ[2] * math.copysign(1.0, terms[k].coefficient) * btot)]
+            else:
+                pairs = [(k, occ[2] * t.coefficient) for k, t in enumerate(terms)]
+            for k, w in pairs:
+                if w == 0.0:
+                    continue
+                m = -1
+                if cfg.sample_cost_terms:
+                    if ctot == 0.0:
+                        degenerate = True
+                        continue
+                    m = int(rng.choice(len(cost), p=cmass / ctot))
+                evals.append((i, oi, k, m, cw * w, counter))
+                counter += 1
+    return evals, degenerate
+
+
 def stochastic_ps_grad(req: GradRequest, cfg: StochasticConfig, evaluator=None) -> GradResult:
     """ref gradients.py:168-174 / :241-326: Monte-Carlo PS over generator terms, cost terms
-    and coordinates with importance weights; substreams keyed exactly as the reference."""
-    from .sampling import philox_key  # noqa: F401  (keeps the RNG module loaded)
+    and coordinates with importance weights; substreams keyed exactly as the reference.
 
+    Without a custom ``evaluator`` every shifted evaluation of every sample runs in ONE
+    batched launch sequence per observable variant: each shifted circuit is a row of the
+    per-term expansion (:func:`_ps_structure`, one pseudo-parameter column per (gate, term)),
+    and sampled estimators draw row b with seed derive_seed(est.seed, i, +-, counter) exactly as
+    the reference's evaluator does (gradients.py:96-110)."""
     c = req.circuit
     obs = as_pauli_sum(req.observable)
     b = normalize_bindings(req.bindings)
@@ -360,66 +409,92 @@ def stochastic_ps_grad(req: GradRequest, cfg: StochasticConfig, evaluator=None) 
                              "rule does not apply — use finite_difference_grad instead")
         terms = tuple(t for t in gen.terms if t.factors and t.coefficient != 0.0)
         occs.append((j, index[e.symbol], e.coeff, e.coeff * b[e.symbol] + e.const, terms))
-    base = [g.resolved(b) for g in c.gates]
-    ev = GpuEvaluator(req.estimator) if evaluator is None else evaluator
-    start = ev.count
     cost = [t for t in obs.terms if t.factors and t.coefficient != 0.0]
     cmass = np.array([abs(t.coefficient) for t in cost])
     ctot = float(cmass.sum())
     omass = np.array([abs(o[2]) * sum(abs(t.coefficient) for t in o[4]) for o in occs])
     otot = float(omass.sum())
-    degenerate = False
+    evals, degenerate = _stochastic_walk(occs, cost, cmass, ctot, omass, otot, cfg)
+
+    def o_eff(m):
+        if m < 0:
+            return obs
+        return PauliSum([cost[m].with_coefficient(math.copysign(1.0, cost[m].coefficient) * ctot)])
+
+    if evaluator is not None:
+        # custom evaluator protocol: one call per shifted circuit, in the reference's order
+        base = [g.resolved(b) for g in c.gates]
+
+        def shifted(occ, k, delta):
+            j, _, _, v, terms = occ
+            exp = [Gate(t.support, exponent=ParamExpr(None, 0.0, v * t.coefficient + (delta if kk == k else 0.0)),
+                        generator=PauliSum([t.with_coefficient(1.0)])) for kk, t in enumerate(terms)]
+            return Circuit(c.num_qubits, base[:j] + exp + base[j + 1:])
+
+        start = evaluator.count
+        vals = []
+        for i, oi, k, m, w, ctr in evals:
+            fp = evaluator(shifted(occs[oi], k, +SHIFT), o_eff(m), key=(i, 0, ctr))
+            fm = evaluator(shifted(occs[oi], k, -SHIFT), o_eff(m), key=(i, 1, ctr))
+            vals.append((fp, fm))
+        n_eval = evaluator.count - start
+    else:
+        vals = _stochastic_batched(c, syms, b, occs, evals, o_eff, req.estimator)
+        n_eval = 2 * len(evals)
     acc = np.zeros(len(syms))
-
-    def shifted(occ, k, delta):
-        j, _, _, v, terms = occ
-        exp = [Gate(t.support, exponent=ParamExpr(None, 0.0, v * t.coefficient + (delta if kk == k else 0.0)),
-                    generator=PauliSum([t.with_coefficient(1.0)])) for kk, t in enumerate(terms)]
-        return Circuit(c.num_qubits, base[:j] + exp + base[j + 1:])
-
-    for i in range(cfg.num_samples):
-        rng = np.random.Generator(np.random.Philox(np.random.SeedSequence(cfg.seed, spawn_key=(i,))))
-        counter = 0
-        smp = np.zeros(len(syms))
-        if cfg.sample_coordinates:
-            if otot == 0.0:
-                degenerate, chosen = True, []
-            else:
-                pr = omass / otot
-                pick = int(rng.choice(len(occs), p=pr))
-                chosen = [(occs[pick], 1.0 / pr[pick])]
-        else:
-            chosen = [(o, 1.0) for o in occs]
-        for occ, cw in chosen:
-            terms = occ[4]
-            btot = sum(abs(t.coefficient) for t in terms)
-            if cfg.sample_generator_terms:
-                if btot == 0.0:
-                    degenerate = True
-                    continue
-                k = int(rng.choice(len(terms), p=np.array([abs(t.coefficient) for t in terms]) / btot))
-                pairs = [(k, occ[2] * math.copysign(1.0, terms[k].coefficient) * btot)]
-            else:
-                pairs = [(k, occ[2] * t.coefficient) for k, t in enumerate(terms)]
-            for k, w in pairs:
-                if w == 0.0:
-                    continue
-                if cfg.sample_cost_terms:
-                    if ctot == 0.0:
-                        degenerate = True
-                        continue
-                    m = int(rng.choice(len(cost), p=cmass / ctot))
-                    o_eff = PauliSum([cost[m].with_coefficient(math.copysign(1.0, cost[m].coefficient) * ctot)])
-                else:
-                    o_eff = obs
-                fp = ev(shifted(occ, k, +SHIFT), o_eff, key=(i, 0, counter))
-                fm = ev(shifted(occ, k, -SHIFT), o_eff, key=(i, 1, counter))
-                counter += 1
-                smp[occ[1]] += cw * w * (fp - fm)
+    smp = np.zeros(len(syms))
+    cur = 0
+    for (i, oi, k, m, w, ctr), (fp, fm) in zip(evals, vals):
+        while cur < i:          # the reference adds each sample's vector to acc in order
+            acc += smp
+            smp = np.zeros(len(syms))
+            cur += 1
+        smp[occs[oi][1]] += w * (fp - fm)
+    while cur < cfg.num_samples:
         acc += smp
+        smp = np.zeros(len(syms))
+        cur += 1
     g = acc / cfg.num_samples
     _finite(g)
-    return GradResult(g, ev.count - start, degenerate)
+    return GradResult(g, n_eval, degenerate)
+
+
+def _stochastic_batched(c, syms, b, occs, evals, o_eff, estimator):
+    """(f+, f-) for every walk entry: all shifted circuits as rows of the per-term expansion,
+    one batched execution per observable variant."""
+    from .ops import expectation as op_expectation
+    from .ops import sampled_expectation as op_sampled
+
+    if not evals:
+        return []
+    ec, names, spec, _ = _ps_structure(c, syms)
+    theta = np.array([b[s] for s in syms], dtype=np.float64)
+    base = np.array([(co * theta[si] + cst) * beta for si, co, cst, beta in spec], dtype=np.float64)
+    col0, off = [], 0                      # first pseudo column of each occurrence
+    for occ in occs:
+        col0.append(off)
+        off += len(occ[4])
+    R = 2 * len(evals)
+    rows = np.repeat(base[None, :], R, axis=0)
+    for r, (i, oi, k, m, w, ctr) in enumerate(evals):
+        rows[2 * r, col0[oi] + k] += SHIFT
+        rows[2 * r + 1, col0[oi] + k] -= SHIFT
+    rows32 = rows.astype(np.float32)
+    out = np.empty(R)
+    by_m: dict = {}
+    for r, e in enumerate(evals):
+        by_m.setdefault(e[3], []).append(r)
+    for m, rs in by_m.items():
+        ix = np.array([[2 * r, 2 * r + 1] for r in rs], dtype=np.int64).reshape(-1)
+        if _is_sampled(estimator):
+            seeds = []
+            for r in rs:
+                i, _, _, _, _, ctr = evals[r]
+                seeds += [derive_seed(estimator.seed, i, 0, ctr), derive_seed(estimator.seed, i, 1, ctr)]
+            out[ix] = op_sampled(ec, names, rows32[ix], [o_eff(m)], estimator.shots, seed=seeds)[:, 0]
+        else:
+            out[ix] = op_expectation(ec, names, rows32[ix], [o_eff(m)])[:, 0]
+    return [(out[2 * r], out[2 * r + 1]) for r in range(len(evals))]
 
 
 class StochasticShift:

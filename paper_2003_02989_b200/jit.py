@@ -834,7 +834,6 @@ class JitProgram:
         self.rows_shift = prog.n - prog.L
         self.block = (C.c_uint32 * P)(*[g[0] for g in geo])
         self.smem = (C.c_uint32 * P)(*[g[1] for g in geo])
-        self.grid = (C.c_uint32 * P)()
         self.prog = prog
         self._remote = {}
         self.persist = PERSIST
@@ -873,9 +872,10 @@ class JitProgram:
                              n_slots=self.prog.n_slots, tiles_log2=self.rows_shift, pad=rows,
                              psi_src=srcs[i] if srcs else 0, skip_psi=int(bool(skip_psi)))
             total = rows << self.rows_shift
-            self.grid[i] = min(total, self.resident[i]) if self.persist else total
+            # a per-call grid array: JitPrograms are shared across threads and batch sizes
+            grid = (C.c_uint32 * 1)(min(total, self.resident[i]) if self.persist else total)
             nat.check(lib.qf_jit_run(C.addressof(self.funcs) + C.sizeof(C.c_void_p) * i,
-                                     C.addressof(self.grid) + 4 * i, C.addressof(self.block) + 4 * i,
+                                     grid, C.addressof(self.block) + 4 * i,
                                      C.addressof(self.smem) + 4 * i, 1, stream, C.byref(args), C.sizeof(args)))
 
     def run(self, rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first=0, last=None,
@@ -901,11 +901,12 @@ class JitProgram:
                 nat.check(lib.qf_jit_run(funcs, grid, block, sm, 1, stream, C.byref(args), C.sizeof(args)))
                 return
         total = rows << self.rows_shift
-        for i in range(self.n):
-            self.grid[i] = min(total, self.resident[i]) if self.persist else total
         cnt = last - first
+        # a per-call grid array: JitPrograms are shared across threads and batch sizes
+        grid = (C.c_uint32 * cnt)(*[min(total, self.resident[i]) if self.persist else total
+                                    for i in range(first, last)])
         nat.check(lib.qf_jit_run(C.addressof(self.funcs) + C.sizeof(C.c_void_p) * first,
-                                 C.addressof(self.grid) + 4 * first, C.addressof(self.block) + 4 * first,
+                                 grid, C.addressof(self.block) + 4 * first,
                                  C.addressof(self.smem) + 4 * first, cnt, stream, C.byref(args), C.sizeof(args)))
 
 

@@ -16,10 +16,13 @@ and the gradient of ``quantum_backward`` (graph.py:471-513) for the adjoint.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
 from . import gates as lib_gates
+from . import planner as pl
 from .circuit import Circuit
 from .engine import ENGINE, UniformBatch
 from .pauli import as_pauli_sum
@@ -46,7 +49,7 @@ def _prep(circuits, symbol_values, symbol_names):
 
 def _to_dev(vals, dev):
     if vals.is_cuda:
-        return vals.to(dtype=torch.float32).contiguous()
+        return vals.to(device=dev, dtype=torch.float32).contiguous()
     if vals.dtype != torch.float32:
         vals = vals.to(torch.float32)
     return vals.to(dev, non_blocking=vals.is_pinned()).contiguous()
@@ -56,14 +59,142 @@ def _out(t, on_dev):
     return t if on_dev else t.cpu().numpy()
 
 
+# ---------------------------------------------------------------------------
+# row partitioning: one launch sequence per (topology, device)
+# ---------------------------------------------------------------------------
+
+_DEVICES: list | None = None
+# a part must move at least this many amplitudes per device before a batch is split
+SPLIT_MIN_AMPS = 1 << 22
+
+
+def set_devices(devices) -> None:
+    """Devices every ``ops.*`` call splits its rows over (one host process
+    drives all GPUs; rows are independent, so the split needs no collective).  ``None``
+    restores the default: ``QF_DEVICES`` ("all" or "0,1,...") or the current device."""
+    global _DEVICES
+    _DEVICES = None if devices is None else [torch.device("cuda", int(getattr(d, "index", d) or 0))
+                                             for d in devices]
+
+
+def devices() -> list:
+    if _DEVICES is not None:
+        return list(_DEVICES)
+    from .engine import _require_cuda
+
+    env = os.environ.get("QF_DEVICES", "")
+    if env:
+        _require_cuda(None)
+        ids = range(torch.cuda.device_count()) if env == "all" else [int(x) for x in env.split(",") if x]
+        return [torch.device("cuda", i) for i in ids]
+    return [_require_cuda(None)]
+
+
+def _subset(circuits, idx):
+    if isinstance(circuits, UniformBatch):
+        return UniformBatch(circuits.circuit, len(idx))
+    return [circuits[i] for i in idx]
+
+
+def topology_groups(circuits, symbol_names) -> list:
+    """Row-index arrays of the rows that share one topology (first-row order), so a batch
+    whose rows differ in structure -- e.g. the reference QCNN app's per-row data circuits
+    (apps/qcnn.py task_circuits) -- runs as one launch sequence per topology."""
+    from .planner import topology_key
+
+    index = {s: i for i, s in enumerate(symbol_names)}
+    keys: dict = {}
+    memo: dict = {}
+    for b, c in enumerate(circuits):
+        k = memo.get(id(c))
+        if k is None:
+            try:
+                k = topology_key(c, index)
+            except KeyError as exc:
+                raise KeyError(f"missing binding for symbol {exc.args[0]!r}") from None
+            memo[id(c)] = k
+        keys.setdefault(k, []).append(b)
+    return [np.asarray(v, dtype=np.int64) for v in keys.values()]
+
+
+def _split(rows: int, n_amps: int, n_dev: int) -> list:
+    if n_dev <= 1 or rows < 2:
+        return [(0, rows)]
+    k = int(min(n_dev, rows, max(1, (rows * n_amps) // SPLIT_MIN_AMPS)))
+    base, extra = divmod(rows, k)
+    out, s = [], 0
+    for r in range(k):
+        e = s + base + (1 if r < extra else 0)
+        out.append((s, e))
+        s = e
+    return out
+
+
+def _run(circuits, symbol_names, vals, observables=(), *, want_grad=False, want_state=False,
+         want_expect=True, upstream=None, post=None, keys=("expectations",)):
+    """Bind + execute ``circuits`` (B rows) split by topology and over :func:`devices`.
+    ``post(out, bound, rows)`` (optional) maps one part's outputs, on its device, to the
+    tensors to return; row-ordered results land on the device of ``vals`` (or the first
+    device).  Launches on different devices overlap: each part is issued asynchronously
+    on its device's current stream before any result is gathered."""
+    B = len(circuits)
+    devs = devices()
+    n = circuits[0].num_qubits
+    groups = [None]
+    while True:
+        parts = []
+        for g in groups:
+            rows = B if g is None else len(g)
+            for a, b in _split(rows, 1 << max(n, 10), len(devs)):
+                idx = None if (g is None and a == 0 and b == B) else \
+                    (np.arange(a, b, dtype=np.int64) if g is None else g[a:b])
+                parts.append(idx)
+        outs = []
+        try:
+            for j, idx in enumerate(parts):
+                d = devs[j % len(devs)] if len(devs) > 1 else devs[0]
+                sub = circuits if idx is None else _subset(circuits, idx)
+                with torch.cuda.device(d):
+                    bound = ENGINE.bind(sub, symbol_names, observables, want_grad=want_grad, device=d,
+                                        want_state=want_state)
+                    v = vals if idx is None else vals[torch.as_tensor(idx, device=vals.device)]
+                    up = None
+                    if upstream is not None:
+                        up = upstream if idx is None else np.asarray(upstream)[idx]
+                    out = bound.execute(_to_dev(v, d), upstream=up, want_grad=want_grad, want_state=want_state,
+                                        want_expect=want_expect)
+                    if post is not None:
+                        out = post(out, bound, idx)
+                outs.append((idx, d, out))
+            break
+        except pl.TopologyMismatch:
+            if groups != [None]:
+                raise
+            groups = topology_groups(circuits, symbol_names)
+    home = vals.device if vals.is_cuda else devs[0]
+    if len(outs) == 1 and outs[0][0] is None and outs[0][1] == home:
+        return outs[0][2]
+    res = {}
+    for key in keys:
+        first = outs[0][2][key]
+        full = torch.empty((B,) + tuple(first.shape[1:]), dtype=first.dtype, device=home)
+        for idx, d, out in outs:
+            part = out[key].to(home, non_blocking=True)
+            if idx is None:
+                full.copy_(part)
+            else:
+                full[torch.as_tensor(idx, device=home)] = part
+        res[key] = full
+    return res
+
+
 def expectation(circuits, symbol_names, symbol_values, operators):
     """[B, n_obs] exact expectations (float64)."""
     circuits, vals, B, on_dev = _prep(circuits, symbol_values, symbol_names)
     ops = [as_pauli_sum(o) for o in operators]
     if B == 0:
         return np.zeros((0, len(ops)))
-    bound = ENGINE.bind(circuits, symbol_names, ops)
-    out = bound.execute(_to_dev(vals, bound.device))
+    out = _run(circuits, symbol_names, vals, ops)
     return _out(out["expectations"], on_dev)
 
 
@@ -74,8 +205,8 @@ def expectation_and_gradient(circuits, symbol_names, symbol_values, operators, u
     ops = [as_pauli_sum(o) for o in operators]
     if B == 0:
         return np.zeros((0, len(ops))), np.zeros((0, len(symbol_names)))
-    bound = ENGINE.bind(circuits, symbol_names, ops, want_grad=True)
-    out = bound.execute(_to_dev(vals, bound.device), upstream=upstream, want_grad=True)
+    out = _run(circuits, symbol_names, vals, ops, want_grad=True, upstream=upstream,
+               keys=("expectations", "grad"))
     return _out(out["expectations"], on_dev), _out(out["grad"], on_dev)
 
 
@@ -93,6 +224,21 @@ def expectation_and_ps_gradient(circuits, symbol_names, symbol_values, operators
     S = len(symbol_names)
     if B == 0:
         return np.zeros((0, len(ops))), np.zeros((0, S))
+    if not isinstance(circuits, UniformBatch) and any(c is not circuits[0] for c in circuits):
+        groups_t = topology_groups(circuits, symbol_names)
+        if len(groups_t) > 1:   # one batched parameter-shift sweep per topology
+            e_all = np.zeros((B, len(ops)))
+            g_all = np.zeros((B, S))
+            up_np = None if upstream is None else np.asarray(upstream, dtype=np.float64).reshape(B, -1)
+            vals_h = vals.detach().cpu()
+            for g in groups_t:
+                e_g, g_g = expectation_and_ps_gradient([circuits[i] for i in g], symbol_names,
+                                                       vals_h[torch.as_tensor(g)], ops,
+                                                       None if up_np is None else up_np[g], chunk_amps)
+                e_all[g], g_all[g] = e_g, g_g
+            if on_dev:
+                return torch.as_tensor(e_all, device=vals.device), torch.as_tensor(g_all, device=vals.device)
+            return e_all, g_all
     vals_np = vals.detach().cpu().numpy().astype(np.float32).astype(np.float64).reshape(B, -1)
     col = {s: i for i, s in enumerate(symbol_names)}
     e0 = expectation(circuits, symbol_names, vals, ops)
@@ -159,8 +305,7 @@ def expectation_and_ps_gradient(circuits, symbol_names, symbol_values, operators
 def state(circuits, symbol_names, symbol_values):
     """[B, 2^n] complex64 final states (device tensor; numpy complex64 for host inputs)."""
     circuits, vals, B, on_dev = _prep(circuits, symbol_values, symbol_names)
-    bound = ENGINE.bind(circuits, symbol_names, [])
-    out = bound.execute(_to_dev(vals, bound.device), want_state=True, want_expect=False)
+    out = _run(circuits, symbol_names, vals, want_state=True, want_expect=False, keys=("state",))
     return _out(out["state"], on_dev)
 
 
@@ -178,19 +323,27 @@ def _row_seeds(seed, B):
     return [derive_seed(int(seed), b) for b in range(B)]
 
 
+def _state_for_sampling(out, bound):
+    n, n_eff = bound.plan.n, bound.plan.n_eff
+    return out["state"] if n_eff == n else _padded(out["state"], n_eff), n_eff
+
+
 def sample(circuits, symbol_names, symbol_values, repetitions: int, seed=0):
     """Bitstrings [B, repetitions, n] uint8 (column q = qubit q); row b draws with
     substream(seed_b) where seed_b = seed[b] or derive_seed(seed, b) (ref sim.py:223-227)."""
     if repetitions < 1:
         raise ValueError("shots must be >= 1")
     circuits, vals, B, on_dev = _prep(circuits, symbol_values, symbol_names)
-    bound = ENGINE.bind(circuits, symbol_names, [])
-    out = bound.execute(_to_dev(vals, bound.device), want_state=True, want_expect=False)
-    n = bound.plan.n
-    psi = out["state"] if bound.plan.n_eff == n else _padded(out["state"], bound.plan.n_eff)
-    keys = [philox_key(s) for s in _row_seeds(seed, B)]
-    idx, _ = sample_indices(psi, bound.plan.n_eff, repetitions, keys)
-    return bits_from_indices(idx.cpu().numpy(), n)
+    seeds = _row_seeds(seed, B)
+
+    def draw(out, bound, idx):
+        psi, n_eff = _state_for_sampling(out, bound)
+        rows = range(B) if idx is None else idx
+        idx_t, _ = sample_indices(psi, n_eff, repetitions, [philox_key(seeds[r]) for r in rows])
+        return {"idx": idx_t}
+
+    out = _run(circuits, symbol_names, vals, want_state=True, want_expect=False, post=draw, keys=("idx",))
+    return bits_from_indices(out["idx"].cpu().numpy(), circuits[0].num_qubits)
 
 
 def _padded(st, n_eff):
@@ -216,7 +369,7 @@ def sampled_expectation(circuits, symbol_names, symbol_values, operators, repeti
     """[B, n_obs] shot estimates with the reference's per-term semantics: term k of an
     operator is measured in its own rotated basis with substream(seed_b, k)
     (ref sim.py:245-272; seed_b as in :func:`sample`).  Terms sharing a basis rotation
-    share one simulated state."""
+    share one simulated state; all terms of a basis are drawn by one sampler launch."""
     if repetitions < 1:
         raise ValueError("shots_per_term must be >= 1")
     circuits, vals, B, on_dev = _prep(circuits, symbol_values, symbol_names)
@@ -238,15 +391,27 @@ def sampled_expectation(circuits, symbol_names, symbol_values, operators, repeti
     values_per_term: dict = {}
     for sig, members in groups.items():
         extra = _basis_gates(members[0][2].__class__(1.0, dict(sig))) if sig else []
-        rot = [Circuit(c.num_qubits, tuple(c.gates) + tuple(extra)) for c in circuits] if extra else circuits
-        bound = ENGINE.bind(rot, symbol_names, [])
-        st = bound.execute(_to_dev(vals, bound.device), want_state=True, want_expect=False)["state"]
-        n, n_eff = bound.plan.n, bound.plan.n_eff
-        psi = st if n_eff == n else _padded(st, n_eff)
+        if extra:
+            rot = [Circuit(c.num_qubits, tuple(c.gates) + tuple(extra)) for c in
+                   ([circuits.circuit] if isinstance(circuits, UniformBatch) else circuits)]
+            rot = UniformBatch(rot[0], B) if isinstance(circuits, UniformBatch) else rot
+        else:
+            rot = circuits
+        # every term of this basis draws from the same state: the state is repeated once per
+        # term as sampler rows (keys substream(seed_b, k)), one launch for all of them
+        ks = sorted({k for _, k, _ in members})
+
+        def draw(out, bound, idx, ks=ks):
+            psi, n_eff = _state_for_sampling(out, bound)
+            rows = list(range(B)) if idx is None else list(idx)
+            keys = [philox_key(seeds[r], k) for r in rows for k in ks]
+            idx_t, _ = sample_indices(psi.contiguous(), n_eff, repetitions, keys, keys_per_row=len(ks))
+            return {"idx": idx_t.reshape(len(rows), len(ks), repetitions)}
+
+        out = _run(rot, symbol_names, vals, want_state=True, want_expect=False, post=draw, keys=("idx",))
+        idx_all = out["idx"].cpu().numpy()                      # [B, len(ks), shots]
         for oi, k, t in members:
-            keys = [philox_key(seeds[b], k) for b in range(B)]
-            idx, _ = sample_indices(psi, n_eff, repetitions, keys)
-            idx = idx.cpu().numpy()
+            idx = idx_all[:, ks.index(k), :]
             mask = 0
             for q in t.factors:
                 mask |= 1 << q

@@ -172,6 +172,11 @@ def _class_ok(cls: int, m) -> bool:
     return bool(m[0, 0].imag == 0 and m[1, 1].imag == 0 and m[0, 1].real == 0 and m[1, 0].real == 0)
 
 
+class TopologyMismatch(ValueError):
+    """Rows of one bound batch differ in gate structure (ops.* then splits the batch into
+    one launch sequence per topology)."""
+
+
 def batch_overrides(template, circuits, symbol_index, infos) -> dict:
     """Rows of one plan must share the template's gate structure (targets, symbols,
     generators, diagonal-ness); concrete values may differ.  Returns {gate index: (cls,
@@ -184,7 +189,7 @@ def batch_overrides(template, circuits, symbol_index, infos) -> dict:
             continue
         seen.add(id(c))
         if c.num_qubits != template.num_qubits or len(c.gates) != len(template.gates):
-            raise ValueError("all circuits of a batch must share one gate structure")
+            raise TopologyMismatch("all circuits of a batch must share one gate structure")
         for i, (gc, gt) in enumerate(zip(c.gates, template.gates)):
             if gc is gt:
                 continue
@@ -213,7 +218,7 @@ def batch_overrides(template, circuits, symbol_index, infos) -> dict:
                     if (cls, ax) != (info.cls, info.axis):
                         over[i] = (cls, ax)
             if bad:
-                raise ValueError(f"gate {i} of a batch row differs in structure from the first row's "
+                raise TopologyMismatch(f"gate {i} of a batch row differs in structure from the first row's "
                                  "(targets, generator, symbol, diagonal-ness); rows of one call must share "
                                  "a topology")
     return over

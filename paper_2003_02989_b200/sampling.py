@@ -36,23 +36,26 @@ def derive_seed(seed: int, *path: int) -> int:
     return int(np.random.SeedSequence(int(seed), spawn_key=tuple(int(p) for p in path)).generate_state(1, np.uint64)[0])
 
 
-def sample_indices(psi: torch.Tensor, n_eff: int, shots: int, keys, stream=None):
-    """psi: [B, 2^n_eff] complex64 on device; keys: [(k0, k1)] per row.
-    Returns (indices [B, shots] int64 device tensor, near-boundary counts [B] int32)."""
+def sample_indices(psi: torch.Tensor, n_eff: int, shots: int, keys, stream=None, keys_per_row: int = 1):
+    """psi: [B, 2^n_eff] complex64 on device; keys: [(k0, k1)] per row (``keys_per_row`` > 1:
+    row-major [B, keys_per_row] keys, every key of a row drawing from that row's CDF).
+    Returns (indices [B, shots] -- [B, keys_per_row, shots] when keys_per_row > 1 -- int64
+    device tensor, near-boundary counts int32)."""
     if shots < 1:
         raise ValueError("shots must be >= 1")
     lib = nat.load()
     B = psi.shape[0]
+    K = int(keys_per_row)
     dev = psi.device
     if stream is None:
         stream = torch.cuda.current_stream(dev).cuda_stream
-    kt = torch.tensor(np.array(keys, dtype=np.uint64).reshape(B, 2).view(np.int64), device=dev)
+    kt = torch.tensor(np.array(keys, dtype=np.uint64).reshape(B * K, 2).view(np.int64), device=dev)
     nchunk = (1 << n_eff) // 1024
     scratch = torch.empty(B * (2 * nchunk + 1) + 8, dtype=torch.float64, device=dev)
-    idx = torch.empty((B, shots), dtype=torch.int64, device=dev)
-    near = torch.zeros(B, dtype=torch.int32, device=dev)
-    nat.check(lib.qf_sample(psi.data_ptr(), n_eff, B, shots, kt.data_ptr(), scratch.data_ptr(), idx.data_ptr(),
-                            near.data_ptr(), stream))
+    idx = torch.empty((B, K, shots) if K > 1 else (B, shots), dtype=torch.int64, device=dev)
+    near = torch.zeros(B * K, dtype=torch.int32, device=dev)
+    nat.check(lib.qf_sample_multi(psi.data_ptr(), n_eff, B, K, shots, kt.data_ptr(), scratch.data_ptr(),
+                                  idx.data_ptr(), near.data_ptr(), stream))
     return idx, near
 
 

@@ -270,7 +270,7 @@ def expectation(state: StateVector, obs) -> float:
     """Exact <state|obs|state> (ref sim.py:203-213): identity terms exact, pairwise term sum."""
     obs = as_pauli_sum(obs)
     plain = [t for t in obs.terms if t.factors]
-    vals = _term_values_dev(state.device_amplitudes().reshape(1, -1), state.num_qubits, plain)[0].cpu().numpy() \
+    vals = _term_values_dev(_device_amps(state).reshape(1, -1), state.num_qubits, plain)[0].cpu().numpy() \
         if plain else []
     parts = []
     k = 0
@@ -303,7 +303,9 @@ def batch_execute(circuits, bindings_matrix, observables) -> np.ndarray:
         _check_cap(c.num_qubits)
         from .planner import topology_key
 
-        key = topology_key(c, {s: k for k, s in enumerate(syms)})
+        # the symbol names are part of the key: two circuits of one structure but different
+        # symbol names bind different columns of their own rows
+        key = (topology_key(c, {s: k for k, s in enumerate(syms)}), tuple(syms))
         groups.setdefault(key, ([], [], syms))
         groups[key][0].append(i)
         groups[key][1].append(row)
@@ -321,8 +323,21 @@ def batch_execute(circuits, bindings_matrix, observables) -> np.ndarray:
 # ---------------------------------------------------------------------------
 
 
-def _padded_dev(state: StateVector):
-    a = state.device_amplitudes().reshape(1, -1)
+def _device_amps(state) -> torch.Tensor:
+    """complex64 device amplitudes of a StateVector of this package, or of any object with the
+    reference StateVector's ``num_qubits`` / ``amplitudes`` (ref sim.py:38-69) -- e.g. one a
+    user built with qcflow itself before ``install()`` rebound the module."""
+    dev_amps = getattr(state, "device_amplitudes", None)
+    if dev_amps is not None:
+        return dev_amps()
+    a = np.asarray(state.amplitudes)
+    if a.shape != (2 ** int(state.num_qubits),):
+        raise ValueError(f"expected {2 ** int(state.num_qubits)} amplitudes, got shape {a.shape}")
+    return torch.as_tensor(a, dtype=torch.complex64).to(torch.device("cuda", torch.cuda.current_device()))
+
+
+def _padded_dev(state):
+    a = _device_amps(state).reshape(1, -1)
     n = state.num_qubits
     n_eff = max(n, 10)
     if n_eff != n:
