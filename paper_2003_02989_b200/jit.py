@@ -52,6 +52,10 @@ GS_THREAD_BYTES = int(os.environ.get("QF_GS_BYTES", str(40 * 1024)))
 # the next tile into shared memory with cp.async while computing the current one
 PERSIST_MODE = int(os.environ.get("QF_PERSIST", "0") or 0)
 PERSIST = PERSIST_MODE > 0
+# timing experiments only (results are WRONG): "noload" -- tiles start from register values
+# derived from the thread index instead of global loads; "nocompute" -- stages do no gate
+# arithmetic (exchanges, loads and stores stay); "memonly" -- loads and stores only
+EXP_MODE = os.environ.get("QF_EXP", "")
 
 
 def _flit(x: float) -> str:
@@ -429,6 +433,11 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             if adj and init == pl.INIT_LOAD:
                 w("  const float2* __restrict__ lt0 = lam + gt0;")
             for r in range(NR):
+                if EXP_MODE == "noload":
+                    w(f"  v0[{r}] = make_float2((float)(gt0 + {r}u) * 1e-9f, 0.5f);")
+                    if adj:
+                        w(f"  v1[{r}] = make_float2(0.25f, (float)(gt0 ^ {r}u) * 1e-9f);")
+                    continue
                 w(f"  v0[{r}] = pt0[{roff(st0, r)}ll];")
                 if adj:
                     w(f"  v1[{r}] = " + (f"lt0[{roff(st0, r)}ll];" if init == pl.INIT_LOAD else
@@ -468,7 +477,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             staging = [ln for ln in o[mark_stage:mark_ptr] if ln not in vdecl]
             o[mark_stage:mark_load_end] = (vdecl + o[mark_ptr:mark_ptr_end] + o[mark_load:mark_load_end] + staging)
         # ---- stages ----
-        for si, st in enumerate(st_rows):
+        for si, st in enumerate(st_rows if EXP_MODE != "memonly" else []):
             if si:
                 prev = st_rows[si - 1]
                 if si > 1 or PERSIST:
@@ -494,7 +503,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 w(f"  {{ const u32 gt = base | {_xor_expr(tglob(st))};")
             else:
                 w("  {")
-            for k in range(int(st[48]), int(st[49])):
+            for k in (range(int(st[48]), int(st[49])) if EXP_MODE != "nocompute" else []):
                 op = prog.ops[k]
                 kind = int(op[0])
                 s0, s1, moff = int(op[1]), int(op[2]), int(op[3]) - mb
