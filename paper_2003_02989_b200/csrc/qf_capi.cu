@@ -456,9 +456,18 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
       const uint32_t bit = 1u << q0;
       const int ax = (x & bit) ? 1 : 0, bz = (z & bit) ? 1 : 0;
       const int flip = kind == 1 ? bz : (ax ^ bz);
+      // merged slot (E[7]: 1 head, 2 member): the head writes the slot scale, every member
+      // its scale relative to the head next to tau (the kernel weights its gradient by it)
+      float rel = 0.f;
       if (slot >= 0) {
         const double sc = mp == m ? m : sqrt(m * mp);
-        slot_scale[(size_t)row * n_slots + slot] = flip ? -sc : sc;
+        const double s_ = flip ? -sc : sc;
+        if (E[7] == 2) {
+          rel = (float)(s_ / slot_scale[(size_t)row * n_slots + slot]);
+        } else {
+          slot_scale[(size_t)row * n_slots + slot] = s_;
+          rel = 1.f;
+        }
       }
       Z u00 = {M[off].x, M[off].y}, u01 = {M[off + 1].x, M[off + 1].y}, u10 = {M[off + 2].x, M[off + 2].y};
       if (adjoint) {  // kernels of the adjoint sweep apply U^dag
@@ -485,7 +494,7 @@ __device__ void frame_walk_row(const int32_t* __restrict__ ev, int n_ev, int adj
         x ^= bit;
         if (kind == 2) z ^= bit;
       }
-      M[off] = make_float2((float)tau, 0.f);
+      M[off] = make_float2((float)tau, rel);
     } else if (kind == 7) {  // normalised two-qubit Pauli-string rotation on (q0 msb, q1 lsb)
       const int code = E[6];
       const int l0 = code & 3, l1 = (code >> 2) & 3;  // 1 X, 2 Y, 3 Z

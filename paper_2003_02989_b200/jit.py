@@ -56,6 +56,13 @@ PERSIST = PERSIST_MODE > 0
 # derived from the thread index instead of global loads; "nocompute" -- stages do no gate
 # arithmetic (exchanges, loads and stores stay); "memonly" -- loads and stores only
 EXP_MODE = os.environ.get("QF_EXP", "")
+# integer-weight phase tables: "f4" 16-byte entries (c, c, -s, s) -- no ALU work per lookup;
+# (measured: "cs" is faster, forward middle passes 0.93 -> 0.86 ms on the headline)
+# "cs" 8-byte (c, s) entries (half the shared-memory bytes, one FADD per lookup)
+TB_MODE = os.environ.get("QF_TB_MODE", "cs")
+# integer-weight phase polynomials evaluated per amplitude in Gray-code order (one live value)
+# instead of by a 2^R-entry Walsh transform
+STREAM_POLY = os.environ.get("QF_STREAM_POLY", "auto")   # auto: R >= 5 (measured: R = 4 keeps the WHT)
 
 
 def _flit(x: float) -> str:
@@ -208,11 +215,20 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         outer = [int(x) for x in p[16:16 + n_out]]
         init_mat = [int(x) for x in p[48:48 + n]]
         mcnt, acnt, ccnt, scnt = me - mb, ae - ab, ce - cb, sle - slb
+        # merged gradient slots (planner MERGE_SLOTS): register accumulators, stored once at
+        # the group's last rotation of the pass
+        pass_op_ids = [k for s_ in range(sb, se) for k in range(int(prog.stages[s_][48]),
+                                                                 int(prog.stages[s_][49]))]
+        merged_last = {}
+        for k_ in pass_op_ids:
+            if adj and int(prog.ops[k_][14]) and int(prog.ops[k_][7]) >= 0:
+                merged_last[int(prog.ops[k_][7])] = k_
         # slot partials: one float per thread and slot, or (many slots) one per warp after a
         # shuffle reduction, so the CTA keeps its occupancy
         per_thread_gs = scnt * NT * 4 <= GS_THREAD_BYTES
         # many slots: a ring of 16 per-thread slots flushed by a 16-value warp transpose-reduction
-        chunked = (not per_thread_gs) and CHUNKED_GS and NT >= 64
+        # (slots must then be stored in slot order: not with merged accumulators)
+        chunked = (not per_thread_gs) and CHUNKED_GS and NT >= 64 and not merged_last
         GSW = NT if (per_thread_gs or chunked) else NT // 32
         ws_floats = (NT // 32) * 32 if (scnt and (per_thread_gs or chunked)) else 0
         gs_slots = min(scnt, 16) if chunked else scnt
@@ -237,7 +253,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 if adj and int(op_[7]) >= 0 and _int_grad(prog, int(op_[4]), int(op_[5]), ip[1]) is None:
                     continue
                 int_tables[k_] = (ip, tbl_bytes)
-                tbl_bytes += (2 * ip[2] + 1) * 16
+                tbl_bytes += (2 * ip[2] + 1) * (8 if TB_MODE == "cs" else 16)
         smem = (smem + 15) // 16 * 16 + tbl_bytes
         prefetch = PERSIST_MODE == 2 and init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI)
         NPF = (2 if (adj and init == pl.INIT_LOAD) else 1) if prefetch else 0
@@ -301,10 +317,13 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         if ws_floats:
             w(f"  float* WS = GS + {gs_slots * GSW};")
         if int_tables:
-            w(f"  float4* TB = reinterpret_cast<float4*>(smem_raw + {(pf_off - tbl_bytes)});")
+            w(f"  {'float2' if TB_MODE == 'cs' else 'float4'}* TB = reinterpret_cast<"
+              f"{'float2' if TB_MODE == 'cs' else 'float4'}*>(smem_raw + {(pf_off - tbl_bytes)});")
         if prefetch:
             w(f"  float2* PF = reinterpret_cast<float2*>(smem_raw + {pf_off});")
         w("  const u32 t = threadIdx.x;")
+        for sl in sorted(merged_last):
+            w(f"  float gm{sl} = 0.f;")
         if PERSIST:
             # persistent CTAs: a contiguous run of tiles each, so the row's staged matrices,
             # angles and phase tables are rebuilt only when the row changes
@@ -371,9 +390,12 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         w("  __syncthreads();")
         if int_tables:
             for k_, ((bcol, ms, H), off) in int_tables.items():
-                w(f"  for (int h = t; h < {2 * H + 1}; h += {NT}) {{ const float2 ph = phase_turns("
-                  f"(int)((u32)(h - {H}) * (u32)ANG[{bcol - ab}]), {'true' if adj else 'false'});"
-                  f" TB[{off // 16} + h] = make_float4(ph.x, ph.x, -ph.y, ph.y); }}")
+                ph = f"phase_turns((int)((u32)(h - {H}) * (u32)ANG[{bcol - ab}]), {'true' if adj else 'false'})"
+                if TB_MODE == "cs":
+                    w(f"  for (int h = t; h < {2 * H + 1}; h += {NT}) TB[{off // 8} + h] = {ph};")
+                else:
+                    w(f"  for (int h = t; h < {2 * H + 1}; h += {NT}) {{ const float2 ph = {ph};"
+                      f" TB[{off // 16} + h] = make_float4(ph.x, ph.x, -ph.y, ph.y); }}")
             w("  __syncthreads();")
         if PERSIST:
             w("  }")
@@ -506,6 +528,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             for k in (range(int(st[48]), int(st[49])) if EXP_MODE != "nocompute" else []):
                 op = prog.ops[k]
                 kind = int(op[0])
+                if EXP_MODE == "nodiag" and kind == pl.OP_DIAG:
+                    continue
                 s0, s1, moff = int(op[1]), int(op[2]), int(op[3]) - mb
                 slot = int(op[7])
                 cls, gk = int(op[9]), int(op[10])
@@ -513,13 +537,20 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     # Pauli-frame normalised rotation: the build step wrote tau (adjoint-ready)
                     ax = 1 if cls == pl.CLS_NX else 2
                     w(f"    {{ const float tau = MM[{moff}].x;")
-                    if adj and slot >= 0 and FUSED_GRAD:
+                    if adj and slot >= 0 and FUSED_GRAD and not int(op[14]):
                         g0 = int(op[8])
                         sc = float(gm[g0 + 4, 0])
                         w("      " + gs_store(slot - slb, f"{_flit(sc)} * gradApplyN<{s0}, {NR}, {gk}, {ax}>(v0, v1, tau)"))
                         w("    }")
                         continue
-                    if adj and slot >= 0:
+                    if adj and slot >= 0 and int(op[14]):
+                        # merged slot: weight = this rotation's frame scale relative to the head
+                        g0 = int(op[8])
+                        sc = float(gm[g0 + 4, 0])
+                        w(f"      gm{slot} = fmaf(MM[{moff}].y, {_flit(sc)} * gradp<{s0}, {NR}, {gk}>(v0, v1), gm{slot});")
+                        if merged_last[slot] == k:
+                            w("      " + gs_store(slot - slb, f"gm{slot}"))
+                    elif adj and slot >= 0:
                         g0 = int(op[8])
                         sc = float(gm[g0 + 4, 0])
                         w("      " + gs_store(slot - slb, f"{_flit(sc)} * gradp<{s0}, {NR}, {gk}>(v0, v1)"))
@@ -615,26 +646,115 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     if kind == pl.OP_DIAG and k in int_tables:
                         (bcol, ms, H), off = int_tables[k]
                         kks = list(range(tb, te))
+                        # h_S = sum_k m_k (-1)^{popc(gx & mask_k)}.  Every term of group S has the
+                        # same register bits (S), whose parity in gx (the Pauli-frame x mask there:
+                        # gt is 0 on register bits) is one sign for the group; the bits outside the
+                        # registers are counted in bulk: sum_k m (1 - 2 bit) = m (K - 2 popc(gx & M))
+                        # for single bits, and with y_d = gx ^ (gx >> d) for pairs at distance d
+                        regmask = sum(1 << q for q in reg_glob)
+                        ydist = {}
+                        hexpr = {}
                         for S, ks in groups.items():
-                            w(f"      int {pre}h{S} = 0;")
+                            const = 0
+                            bulk: dict = {}
+                            rest = []
                             for kk in ks:
-                                m = int(prog.term_mask[kk])
+                                om = int(prog.term_mask[kk]) & ~regmask
                                 mk = ms[kks.index(kk)]
-                                w(f"      {pre}h{S} += (__popc({gv} & {m}u) & 1) ? {-mk} : {mk};")
-                        o.extend(_wht_code({S: f"{pre}h{S}" for S in groups}, R, "int", f"{pre}H", "      "))
-                        if adj and slot >= 0:
+                                bits = [b for b in range(32) if om >> b & 1]
+                                if len(bits) == 0:
+                                    const += mk
+                                elif len(bits) == 1:
+                                    key = ("s", 0, mk)
+                                    bulk.setdefault(key, [0, 0])
+                                    bulk[key][0] |= 1 << bits[0]
+                                    bulk[key][1] += 1
+                                elif len(bits) == 2:
+                                    d = bits[1] - bits[0]
+                                    key = ("p", d, mk)
+                                    bulk.setdefault(key, [0, 0])
+                                    bulk[key][0] |= 1 << bits[0]
+                                    bulk[key][1] += 1
+                                    ydist[d] = True
+                                else:
+                                    rest.append((om, mk))
+                            parts = [str(const)] if const else []
+                            for (typ, d, mk), (msk, cnt) in bulk.items():
+                                srcv = gv if typ == "s" else f"{pre}y{d}"
+                                parts.append(f"{mk} * ({cnt} - 2 * __popc({srcv} & {msk}u))")
+                            for om, mk in rest:
+                                parts.append(f"((__popc({gv} & {om}u) & 1) ? {-mk} : {mk})")
+                            hexpr[S] = " + ".join(parts) or "0"
+                        for d in sorted(ydist):
+                            w(f"      const u32 {pre}y{d} = {gv} ^ ({gv} >> {d});")
+                        for S in groups:
+                            rsm = sum(1 << reg_glob[j] for j in range(R) if S >> j & 1)
+                            if rsm and xcol >= 0:   # frame x bits on the group's register qubits
+                                w(f"      const int {pre}h{S} = ((__popc({gv} & {rsm}u) & 1) ? -1 : 1) * ({hexpr[S]});")
+                            else:
+                                w(f"      const int {pre}h{S} = {hexpr[S]};")
+                        if (R >= 5 if STREAM_POLY == "auto" else STREAM_POLY not in ("0", "", "false")):
+                            # streaming evaluation in Gray-code order: one live h value instead
+                            # of 2^R (register pressure), each step adds the flipped bit's terms
+                            grad_here = adj and slot >= 0
+                            if grad_here:
+                                wb, idm = _int_grad(prog, tb, te, ms)
+                                w("      float gq = 0.f;")
+                            for S in groups:
+                                if S:
+                                    w(f"      const int {pre}t{S} = 2 * {pre}h{S};")
+                            w(f"      int {pre}Hc = {' + '.join(f'{pre}h{S}' for S in groups) or '0'};")
+                            prev = 0
+                            for i in range(NR):
+                                r = i ^ (i >> 1)
+                                if i:
+                                    j = (r ^ prev).bit_length() - 1
+                                    parts = []
+                                    for S in groups:
+                                        if S >> j & 1:
+                                            neg = bin(S & prev).count("1") & 1   # current sign of h_S
+                                            parts.append(("+" if neg else "-") + f"{pre}t{S}")
+                                    if parts:
+                                        w(f"      {pre}Hc = {pre}Hc {' '.join(parts)};")
+                                prev = r
+                                if grad_here:
+                                    hr = f"{pre}Hc" if not idm else f"({pre}Hc - {idm})"
+                                    w(f"      gq = fmaf((float){hr}, im_conj_mul(v1[{r}], v0[{r}]), gq);")
+                                if TB_MODE == "cs":
+                                    w(f"      {{ const float2 T = TB[{off // 8 + H} + {pre}Hc];"
+                                      f" v0[{r}] = cmul_cs(v0[{r}], T);" +
+                                      (f" v1[{r}] = cmul_cs(v1[{r}], T);" if adj else "") + " }")
+                                else:
+                                    w(f"      {{ const float4 T = TB[{off // 16 + H} + {pre}Hc];"
+                                      f" const u64 P = pk(T.x, T.y), N = pk(T.z, T.w);"
+                                      f" v0[{r}] = upk(f2fma(N, pk(v0[{r}].y, v0[{r}].x), f2mul(P, pk(v0[{r}].x, v0[{r}].y))));" +
+                                      (f" v1[{r}] = upk(f2fma(N, pk(v1[{r}].y, v1[{r}].x), f2mul(P, pk(v1[{r}].x, v1[{r}].y))));"
+                                       if adj else "") + " }")
+                            if grad_here:
+                                w("      " + gs_store(slot - slb, f"{_flit(wb)} * gq"))
+                            continue_stream = True
+                        else:
+                            continue_stream = False
+                        if not continue_stream:
+                          o.extend(_wht_code({S: f"{pre}h{S}" for S in groups}, R, "int", f"{pre}H", "      "))
+                        if adj and slot >= 0 and not continue_stream:
                             wb, idm = _int_grad(prog, tb, te, ms)
                             w("      float gq = 0.f;")
                             for r in range(NR):
                                 hr = f"{pre}H{r}" if not idm else f"({pre}H{r} - {idm})"
                                 w(f"      gq = fmaf((float){hr}, im_conj_mul(v1[{r}], v0[{r}]), gq);")
                             w("      " + gs_store(slot - slb, f"{_flit(wb)} * gq"))
-                        for r in range(NR):
-                            w(f"      {{ const float4 T = TB[{off // 16 + H} + {pre}H{r}];"
-                              f" const u64 P = pk(T.x, T.y), N = pk(T.z, T.w);"
-                              f" v0[{r}] = upk(f2fma(N, pk(v0[{r}].y, v0[{r}].x), f2mul(P, pk(v0[{r}].x, v0[{r}].y))));" +
-                              (f" v1[{r}] = upk(f2fma(N, pk(v1[{r}].y, v1[{r}].x), f2mul(P, pk(v1[{r}].x, v1[{r}].y))));"
-                               if adj else "") + " }")
+                        for r in (range(NR) if not continue_stream else []):
+                            if TB_MODE == "cs":
+                                w(f"      {{ const float2 T = TB[{off // 8 + H} + {pre}H{r}];"
+                                  f" v0[{r}] = cmul_cs(v0[{r}], T);" +
+                                  (f" v1[{r}] = cmul_cs(v1[{r}], T);" if adj else "") + " }")
+                            else:
+                                w(f"      {{ const float4 T = TB[{off // 16 + H} + {pre}H{r}];"
+                                  f" const u64 P = pk(T.x, T.y), N = pk(T.z, T.w);"
+                                  f" v0[{r}] = upk(f2fma(N, pk(v0[{r}].y, v0[{r}].x), f2mul(P, pk(v0[{r}].x, v0[{r}].y))));" +
+                                  (f" v1[{r}] = upk(f2fma(N, pk(v1[{r}].y, v1[{r}].x), f2mul(P, pk(v1[{r}].x, v1[{r}].y))));"
+                                   if adj else "") + " }")
                     elif kind == pl.OP_DIAG:
                         if adj and slot >= 0:
                             bnames = {}

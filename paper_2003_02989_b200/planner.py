@@ -61,6 +61,12 @@ GK_P = 4
 INIT_LOAD, INIT_ZERO, INIT_PRODUCT, INIT_LOAD_PSI = 0, 1, 2, 3
 
 STAGE_INTS, OP_INTS, PASS_INTS = 64, 16, 128
+# op row: 0 kind, 1-2 register slots, 3 matrix offset, 4-6 term range / subset table, 7 slot,
+# 8 generator offset, 9 class, 10 generator kind, 11 frame x column, 12 Pauli-string code,
+# 13 block dimension, 14 merged-slot role (1 head, 2 member)
+# measured: two extra live accumulators push the 128-register adjoint kernels into spills
+# (SASS: +35 MOV per amplitude), so merging is off by default
+MERGE_SLOTS = __import__("os").environ.get("QF_MERGE_SLOTS", "0") not in ("0", "", "false")
 
 
 def swizzle(l: int) -> int:
@@ -631,13 +637,30 @@ def plan_stages(p: Pass, R: int) -> None:
     p.stages = stages
 
 
-def stage_slots(p: Pass, st: Stage, R: int):
-    """(register local bits, thread local bits [lanes first])."""
+def stage_slots(p: Pass, st: Stage, R: int, edge: bool = True):
+    """(register local bits, thread local bits [lanes first]).
+
+    Edge stages (a pass's first / last, which load / store global memory) keep the lowest
+    free bits as lanes (local bits 0..3: 128-byte runs).  Inner stages only exchange through
+    shared memory, whose 64-bit accesses are conflict-free when the 16 lanes of a half-warp
+    hit 16 distinct 8-byte bank pairs: with ``swizzle`` the low nibble of local bit b is bit
+    b mod 4, so lanes 0..3 take free bits of four distinct classes mod 4 where possible."""
     L = len(p.qubits)
     rs = set(st.regs)
     free = [b for b in range(L) if b not in rs]
-    # the 5 lowest free tile bits become lane bits (bits 0..LANE_Q-1 whenever free)
-    return list(st.regs), free
+    if edge or CONFLICT_FREE_LANES is False:
+        return list(st.regs), free
+    lanes, seen = [], set()
+    for b in free:
+        if len(lanes) < LANE_Q and b % 4 not in seen:
+            lanes.append(b)
+            seen.add(b % 4)
+    if len(lanes) < LANE_Q:
+        return list(st.regs), free
+    return list(st.regs), lanes + [b for b in free if b not in lanes]
+
+
+CONFLICT_FREE_LANES = __import__("os").environ.get("QF_LANE_ORDER", "1") not in ("0", "", "false")
 
 
 # ---------------------------------------------------------------------------
@@ -911,8 +934,13 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         fwd_index = passes.index(p)
         if frame and adjoint:
             events.append([EV_PASS, -1, -1, -1, -1, -1, fwd_index, 0])
+        # slot merging (adjoint, frame-normalised X/Y rotations): rotations of one pass that
+        # share a symbol and a generator weight accumulate into ONE gradient slot in registers;
+        # each carries its per-row frame scale relative to the group head (written by the
+        # frame walk next to tau), so the slot needs one store and one reduction per tile
+        merge_heads: dict = {}
         for si, st in enumerate(stages):
-            regs, thr = stage_slots(p, st, R)
+            regs, thr = stage_slots(p, st, R, edge=st is p.stages[0] or st is p.stages[-1])
             srow = np.zeros(STAGE_INTS, dtype=np.int32)
             reg_glob = [p.qubits[b] for b in regs]
             srow[0:R] = reg_glob
@@ -987,12 +1015,24 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         if orow[10] != GK_MATRIX:   # single Pauli: its scaled coefficient follows the matrix
                             beta = sum(c for f, c in info.terms if f)
                             em.genmats.extend([2.0 * info.coeff * beta, 0.0])
-                        orow[7] = em.new_slot()
-                        em.grad_slots.setdefault(info.sym, []).append(int(orow[7]))
+                        mkey = None
+                        if frame and MERGE_SLOTS and orow[9] in (CLS_NX, CLS_NY) and orow[10] != GK_MATRIX:
+                            mkey = (info.sym, int(orow[10]), float(np.float32(em.genmats[-2])))
+                        if mkey is not None and mkey in merge_heads:
+                            orow[7] = merge_heads[mkey]
+                            orow[14] = 2                 # member: adds into the head's slot
+                        else:
+                            orow[7] = em.new_slot()
+                            em.grad_slots.setdefault(info.sym, []).append(int(orow[7]))
+                            if mkey is not None:
+                                merge_heads[mkey] = int(orow[7])
+                                orow[14] = 1             # head of a (possibly single) group
                     if ev is not None:
                         ev[4] = int(orow[7])
                         if is_block:
                             ev[7] = block_slots(1 << len(order))   # slots sharing the scale m
+                        elif orow[14]:
+                            ev[7] = int(orow[14])                  # merged slot: 1 head, 2 member
                         events.append(ev)
                 elif op.kind == OP_DIAG:
                     terms = em.diag_terms(op)
