@@ -195,7 +195,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
     env_minb = int(os.environ.get("QF_MINB_ADJ" if adj else "QF_MINB_FWD", "0"))
     # measured best (tools/sweep.sh): 128 registers for the 12/5 forward (4 CTAs x 128
     # threads), 64 for the 12/4 forward, 128 for the 12/4 adjoint (2 CTAs x 256 threads)
-    tuned = {(12, 5, False): 4, (12, 4, False): 4, (12, 4, True): 2}.get((L, R, adj))
+    tuned = {(12, 5, False): 4, (12, 4, False): 4, (12, 4, True): 2, (12, 5, True): 2}.get((L, R, adj))
     minb = env_minb or tuned or max(1, min(8, 65536 // (NT * (NR * 2 * NA + 32))))
     gm = prog.genmats.reshape(-1, 2) if len(prog.genmats) else np.zeros((0, 2), np.float32)
     src = []
