@@ -271,11 +271,11 @@ class Bound:
         over = pl.batch_overrides(template, self.circuits, sym_index, pl.analyse(template, sym_index)) \
             if len(self.circuits) > 1 and not uniform else {}
         # block-fused adjoint (planner.build_ops(block=True)): plan-specialised kernels only
-        block = (want_grad and os.environ.get("QF_BLOCK_ADJ", "1") not in ("0", "", "false")
-                 and _jit.enabled(len(self.circuits), max(n, pl.N_MIN)))
+        jit_on = _jit.enabled(len(self.circuits), max(n, pl.N_MIN))
+        block = (want_grad and os.environ.get("QF_BLOCK_ADJ", "1") not in ("0", "", "false") and jit_on)
         self.plan = engine.plan(template, sym_index, obs, want_grad, self.lam_diag,
                                 tuple(self.hkeys) if want_grad else None, device, from_state, frame, over,
-                                block=block)
+                                block=block, jit=jit_on)
         plan = self.plan
         self.frame = plan.fwd.frame
 
@@ -483,7 +483,8 @@ class Bound:
             else:
                 lam.zero_()
         partials = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
-        ja = ad.jit(dev, B, force=ad.n_blocks > 0)
+        # block-fused and R = 5 adjoint programs exist only as plan-specialised kernels
+        ja = ad.jit(dev, B, force=ad.n_blocks > 0 or ad.prog.R != pl.ADJ_R)
         if ckpt:
             ck = ckpt[0]
             ja.run_ckpt(B, [_ptr(t) for t in reversed(ck)], None, _ptr(lam), _ptr(mats), _ptr(angs), _ptr(hw_t),
@@ -541,11 +542,12 @@ class Engine:
         self._lock = threading.Lock()
 
     def plan(self, template, symbol_index, obs: ObsInfo, adjoint: bool, lam_diag: bool, hkeys, device,
-             from_state: bool = False, frame: bool = False, overrides=None, block: bool = False):
+             from_state: bool = False, frame: bool = False, overrides=None, block: bool = False,
+             jit: bool = False):
         overrides = overrides or {}
         topo = pl.topology_key(template, symbol_index)
         key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state, frame,
-               tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block)
+               tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block, jit)
         with self._lock:
             hit = self._plans.get(key)
             if hit is not None:
@@ -565,7 +567,7 @@ class Engine:
             infos_a = pl.analyse(template, symbol_index, overrides)
             hterms = _TermList([_Term(dict(kk), 1.0) for kk in hkeys])
             adjp = pl.build_program(template, infos_a, n_eff, adjoint=True, observables=[hterms],
-                                    lam_diag=lam_diag, frame=frame, block=block)
+                                    lam_diag=lam_diag, frame=frame, block=block, jit=jit)
         ckpt = False
         if adjp is not None and frame and lam_diag and not from_state and \
                 os.environ.get("QF_CKPT", "1") not in ("0", "", "false"):

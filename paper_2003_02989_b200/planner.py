@@ -838,7 +838,7 @@ def block_slots(D: int) -> int:
 def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool,
                   observables=None, obs_diag_ids=(), lam_diag: bool = False,
                   from_state: bool = False, frame: bool = False, mirror: bool = False,
-                  block: bool = False) -> Program:
+                  block: bool = False, jit: bool = False) -> Program:
     """Plan + emit.  ``observables``: list of PauliSums; ``obs_diag_ids``: those fused as
     OBS ops at the end of the forward program; ``lam_diag``: adjoint with a diagonal H
     whose lambda-init / energy is fused into the first backward pass; ``from_state``:
@@ -857,11 +857,12 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     block = block and (adjoint or mirror)
     ops = build_ops(infos, adjoint or mirror, block=block)
     L, R = geometry(adjoint)
-    if adjoint and "QF_GEOM_ADJ" not in __import__("os").environ and \
+    if adjoint and jit and "QF_GEOM_ADJ" not in __import__("os").environ and \
             all(o.kind in (OP_DENSE1, OP_DIAG, OP_OBS) for o in ops):
         # rotation / phase-polynomial programs (QAOA, HEA): 32 amplitudes of psi and lambda
         # per thread, 2 CTAs x 4 warps per SM -- fewer stage exchanges per gate; measured
-        # on the headline's middle backward passes 2.20 -> 2.13 ms (R = 4: 16 warps per SM)
+        # on the headline's middle backward passes 2.20 -> 2.13 ms (R = 4: 16 warps per SM).
+        # Plan-specialised kernels only (``jit``): the interpreted kernel has R = 4 adjoints
         L, R = ADJ_L, 5
     if mirror:
         L = geometry(True)[0]

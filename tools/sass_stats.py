@@ -51,7 +51,7 @@ def programs(name):
     lam_diag = all(all(p == "Z" for _, p in k) for k in hk)
     adj = pl.build_program(circ, pl.analyse(circ, si), n, adjoint=True,
                            observables=[_TermList([_Term(dict(k), 1.0) for k in hk])], lam_diag=lam_diag,
-                           frame=frame, block=os.environ.get("QF_BLOCK_ADJ", "1") not in ("0", ""))
+                           frame=frame, block=os.environ.get("QF_BLOCK_ADJ", "1") not in ("0", ""), jit=True)
     return fwd, adj
 
 
