@@ -8,6 +8,8 @@ and single-threaded, so run them side by side:
     OPENBLAS_NUM_THREADS=1 python tests/golden/make_config_golden.py cfg3
     OPENBLAS_NUM_THREADS=1 python tests/golden/make_config_golden.py cfg4_0   # ~35 min
     OPENBLAS_NUM_THREADS=1 python tests/golden/make_config_golden.py cfg4_1   # ~35 min
+    OPENBLAS_NUM_THREADS=1 python tests/golden/make_config_golden.py cfg4d_0  # ~2 min (per-term draws)
+    OPENBLAS_NUM_THREADS=1 python tests/golden/make_config_golden.py cfg4d_1
     OPENBLAS_NUM_THREADS=1 python tests/golden/make_config_golden.py cfg5_28  # ~40 min, 28q
     OPENBLAS_NUM_THREADS=1 python tests/golden/make_config_golden.py stoch
 
@@ -166,6 +168,31 @@ def part_cfg4(b):
            {"amp_idx": idx, "amps": st.amplitudes[idx], "bits": bits})
 
 
+def part_cfg4d(b):
+    """cfg4 circuit b, per-term draws of sampled_expectation (sim.py:245-272): sum Z needs no
+    basis change, so term k draws with substream(seed_e, k) from the one simulated state --
+    recorded per term (the reference function only returns their mean) and re-aggregated
+    with the reference's pairwise sum to reproduce its sampled_expectation exactly."""
+    L = _setup()
+    import qcflow
+    from qcflow.rng import derive_seed, substream
+    from qcflow.sim import _draw_bits, _pairwise_sum, simulate
+
+    from paper_2003_02989_b200 import workloads as wl
+
+    t0 = time.time()
+    circ = wl.rcs_circuits(b + 1, 24, 20, lib=L)[b]
+    st = simulate(circ)
+    seed_e = derive_seed(wl.SEED_RCS_SHOTS + 1, b)
+    bits = np.stack([_draw_bits(st, 1000, substream(seed_e, k)) for k in range(24)])   # [24, 1000, 24]
+    idx = (bits.astype(np.int64) << np.arange(24)).sum(axis=2)
+    contrib = [float((1.0 - 2.0 * bits[k, :, k]).mean()) for k in range(24)]
+    _write(f"cfg4d_{b}", {"reference": "qcflow " + qcflow.__version__, "circuit_index": b, "sampled_seed": seed_e,
+                          "sampled_expectation_from_draws": float(_pairwise_sum(contrib)),
+                          "seconds": time.time() - t0},
+           {"term_idx": idx.astype(np.int32)})
+
+
 def part_cfg5_28():
     """cfg5 family at 28 qubits (depth 14, SEED_BIG) with the cap override: sum-Z + amplitudes."""
     os.environ["QCFLOW_MAX_QUBITS"] = "28"
@@ -232,6 +259,8 @@ def main():
     part = sys.argv[1]
     if part.startswith("cfg4_"):
         part_cfg4(int(part.split("_")[1]))
+    elif part.startswith("cfg4d_"):
+        part_cfg4d(int(part.split("_")[1]))
     else:
         globals()["part_" + part]()
 
