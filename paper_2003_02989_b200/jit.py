@@ -697,9 +697,10 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                             # streaming evaluation in Gray-code order: one live h value instead
                             # of 2^R (register pressure), each step adds the flipped bit's terms
                             grad_here = adj and slot >= 0
+                            NQ = 4 if NR >= 16 else 1      # independent gradient chains (ILP)
                             if grad_here:
                                 wb, idm = _int_grad(prog, tb, te, ms)
-                                w("      float gq = 0.f;")
+                                w("      " + " ".join(f"float gq{c} = 0.f;" for c in range(NQ)))
                             for S in groups:
                                 if S:
                                     w(f"      const int {pre}t{S} = 2 * {pre}h{S};")
@@ -719,7 +720,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                                 prev = r
                                 if grad_here:
                                     hr = f"{pre}Hc" if not idm else f"({pre}Hc - {idm})"
-                                    w(f"      gq = fmaf((float){hr}, im_conj_mul(v1[{r}], v0[{r}]), gq);")
+                                    c = i % NQ
+                                    w(f"      gq{c} = fmaf((float){hr}, im_conj_mul(v1[{r}], v0[{r}]), gq{c});")
                                 if TB_MODE == "cs":
                                     w(f"      {{ const float2 T = TB[{off // 8 + H} + {pre}Hc];"
                                       f" v0[{r}] = cmul_cs(v0[{r}], T);" +
@@ -731,7 +733,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                                       (f" v1[{r}] = upk(f2fma(N, pk(v1[{r}].y, v1[{r}].x), f2mul(P, pk(v1[{r}].x, v1[{r}].y))));"
                                        if adj else "") + " }")
                             if grad_here:
-                                w("      " + gs_store(slot - slb, f"{_flit(wb)} * gq"))
+                                tot = " + ".join(f"gq{c}" for c in range(NQ))
+                                w("      " + gs_store(slot - slb, f"{_flit(wb)} * ({tot})"))
                             continue_stream = True
                         else:
                             continue_stream = False
