@@ -87,7 +87,10 @@ typedef struct QfPass {
   int32_t init_mat[32];          /* product init: matrix offset of qubit q's leading 2x2, -1 = |0> */
   int32_t grp_begin, grp_end;    /* subset-boundary tables of this pass */
   int32_t op_begin, op_end;      /* ops of this pass */
-  int32_t pad1[44];
+  int32_t store_pos[16];         /* relabelled passes: physical bit local tile bit i is stored to */
+  int32_t pad1[26];
+  int32_t relabelled;            /* 1: the pass stores its tile permuted (plan-specialised kernels only) */
+  int32_t pad2;
 } QfPass;                        /* 128 x int32 */
 
 /* Everything one pass launch needs; pointers are device pointers. */

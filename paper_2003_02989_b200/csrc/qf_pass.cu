@@ -545,6 +545,10 @@ static int launch_pass(const PassArgs& a, const QfPass& hp, cudaStream_t stream)
 }
 
 int run_pass(const PassArgs& a, const QfPass& hp, bool adj, cudaStream_t stream) {
+  if (hp.relabelled) {  // permuted stores exist only in the plan-specialised kernels (jit.py)
+    set_error("pass %d stores a relabelled tile: run it with the plan-specialised kernels", a.pass);
+    return 2;
+  }
   const int L = a.prog.L, R = a.prog.R;
   if (!adj && R == 5) {
     switch (L) {

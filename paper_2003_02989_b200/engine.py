@@ -389,7 +389,8 @@ class Bound:
         else:
             frame_f = None
         partials = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
-        jf = fw.jit(dev, B, force=remote is not None)
+        # relabelled programs exist only as plan-specialised kernels
+        jf = fw.jit(dev, B, force=remote is not None or fw.prog.final_pos is not None)
         if ckpt:
             ck = ckpt[0]
             jf.run_ckpt(B, [_ptr(t) for t in ck], [0] + [_ptr(t) for t in ck[:-1]], 0, _ptr(mats), _ptr(angs),
@@ -421,6 +422,10 @@ class Bound:
                                               _ptr(expv), 1, stream))
             out["expectations"] = expv
         if want_state:
+            if fw.prog.final_pos is not None:
+                # relabelled program: physical bit final_pos[q] holds qubit q -- one
+                # device-side bit-permuting copy back to the logical layout
+                psi = _unrelabel(psi, fw.prog.final_pos, n_eff)
             st = psi[:, : (1 << plan.n)]
             out["state"] = st.clone() if want_grad else st
         if want_grad:
@@ -533,6 +538,14 @@ def _obs_key(o) -> tuple:
     return tuple((tuple(sorted(t.factors.items())), float(t.coefficient)) for t in s.terms)
 
 
+def _unrelabel(psi: torch.Tensor, final_pos, n: int) -> torch.Tensor:
+    """[B, 2^n] state whose physical bit final_pos[q] is logical qubit q -> logical layout."""
+    B = psi.shape[0]
+    v = psi.reshape([B] + [2] * n)                 # dim 1 + (n - 1 - b) holds physical bit b
+    dims = [0] + [1 + (n - 1 - final_pos[n - 1 - d]) for d in range(n)]
+    return v.permute(dims).contiguous().reshape(B, 1 << n)
+
+
 class Engine:
     def __init__(self, max_bound: int = 64, max_plans: int = 256):
         self._plans: OrderedDict = OrderedDict()
@@ -585,8 +598,11 @@ class Engine:
             if not ckpt:
                 infos = pl.analyse(template, symbol_index, overrides)
         if not ckpt:
+            # jit (qubit relabelling, planner.plan_passes_remap) only without a backward sweep,
+            # which loads the forward's output in the identity layout
             fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
-                                   obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame)
+                                   obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame,
+                                   jit=jit and not adjoint)
         plan = Plan(n, n_eff, len(symbol_index), infos, DeviceProgram(fwd, device), None, lam_diag, obs)
         plan.extra["from_state"] = from_state
         plan.extra["ckpt"] = ckpt

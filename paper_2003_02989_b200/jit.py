@@ -853,6 +853,15 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         # ---- store ----
         if store:
             stl = st_rows[-1]
+            if int(p[126]):
+                # relabelled pass (planner.plan_passes_remap): tile bit at physical position
+                # tileq[i] is stored to physical position p[84 + i]
+                out_of = {tileq[i]: int(p[84 + i]) for i in range(L)}
+                stl = stl.copy()
+                for j in range(R):
+                    stl[j] = out_of[int(stl[j])]
+                for i in range(TB):
+                    stl[8 + i] = out_of[int(stl[8 + i])]
             w(f"  {{ const u32 gs = base | {_xor_expr(tglob(stl))};")
             if pi == remote_pass:
                 SH = n - remote_g

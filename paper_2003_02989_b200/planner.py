@@ -494,11 +494,15 @@ class Stage:
 
 @dataclass
 class Pass:
-    qubits: list          # sorted global qubits of the tile (local bit i -> qubits[i])
+    qubits: list          # logical qubits of the tile, local bit i -> qubits[i] (ascending physical position)
     ops: list
     stages: list = field(default_factory=list)
     init: int = INIT_LOAD
     store: int = 1
+    # qubit relabelling (plan_passes_remap): physical position of every logical qubit when the
+    # pass loads (None: identity), and the physical position local bit i is stored to
+    pos_in: list = None
+    out_pos: list = None
 
 
 class _Sched:
@@ -566,6 +570,88 @@ def plan_passes(ops: list[Op], n: int, L: int) -> list[Pass]:
         passes.append(Pass(sorted(Q), taken))
     if not passes:
         passes.append(Pass(list(range(L)), []))
+    return passes
+
+
+def _sched_copy(sch: "_Sched") -> "_Sched":
+    c = object.__new__(_Sched)
+    c.ops, c.succ = sch.ops, sch.succ
+    c.npred = dict(sch.npred)
+    c.ready = list(sch.ready)
+    c.left = sch.left
+    return c
+
+
+def _greedy_tile(sch: "_Sched", Q: set, L: int) -> list:
+    """The plan_passes greedy on ``sch`` (mutated) from tile ``Q`` (mutated): ops taken."""
+    taken = []
+    while True:
+        taken += sch.drain(lambda o: o.kind in (OP_DIAG, OP_OBS) or set(o.qubits) <= Q)
+        cands = [sch.ops[j] for j in sch.ready]
+        if not cands:
+            break
+        best = min(cands, key=lambda o: (len(set(o.qubits) - Q), o.index))
+        if len(Q | set(best.qubits)) > L:
+            break
+        Q |= set(best.qubits)
+    return taken
+
+
+def _wanted(sch: "_Sched", L: int) -> list:
+    """Qubits the next pass would choose with no lane constraint, in the order it adds them."""
+    c = _sched_copy(sch)
+    Q: set = set()
+    order = []
+    while True:
+        c.drain(lambda o: o.kind in (OP_DIAG, OP_OBS) or set(o.qubits) <= Q)
+        cands = [c.ops[j] for j in c.ready]
+        if not cands:
+            break
+        best = min(cands, key=lambda o: (len(set(o.qubits) - Q), o.index))
+        if len(Q | set(best.qubits)) > L:
+            break
+        for q in best.qubits:
+            if q not in Q:
+                order.append(q)
+        Q |= set(best.qubits)
+    return order
+
+
+def plan_passes_remap(ops: list[Op], n: int, L: int) -> list[Pass]:
+    """plan_passes with qubit relabelling.  Physical bits 0..3 must be tile bits of every pass
+    (lanes 0-15 move 128 contiguous bytes), which in plan_passes wastes 4 of the L tile qubits
+    whenever the pending gates sit on high qubits (brickwork circuits: passes of 6 gates).  Here
+    each pass stores its tile back with a permutation of the tile's physical positions: the
+    qubits the NEXT pass wants (its greedy choice without the lane constraint) are moved onto
+    physical bits 0..3.  Every pass records the layout it loads (pos_in) and the position each
+    local bit is stored to (out_pos); the program's final layout is in Program.final_pos.
+    cfg5 (32 qubits, depth 14, L = 11): 26 -> 15 passes."""
+    if n == L:
+        return plan_passes(ops, n, L)
+    sch = _Sched(ops)
+    pos = list(range(n))          # logical -> physical
+    at = list(range(n))           # physical -> logical
+    passes = []
+    while sch.left > 0:
+        Q = {at[p] for p in range(LANE_Q)}
+        taken = _greedy_tile(sch, Q, L)
+        if not taken:
+            raise AssertionError("pass planner made no progress")
+        want = _wanted(sch, L)
+        for q in want + sorted(range(n), key=lambda q: pos[q]):
+            if len(Q) >= L:
+                break
+            Q.add(q)
+        P = sorted(pos[q] for q in Q)
+        qubits = [at[p] for p in P]
+        nxt = [q for q in want if q in Q][:LANE_Q]
+        order = nxt + [q for q in qubits if q not in nxt]
+        new_pos = {q: P[i] for i, q in enumerate(order)}
+        out_pos = [new_pos[q] for q in qubits]
+        passes.append(Pass(qubits, taken, pos_in=list(pos), out_pos=out_pos))
+        for q, p_ in new_pos.items():
+            pos[q] = p_
+            at[p_] = q
     return passes
 
 
@@ -661,6 +747,9 @@ def stage_slots(p: Pass, st: Stage, R: int, edge: bool = True):
 
 
 CONFLICT_FREE_LANES = __import__("os").environ.get("QF_LANE_ORDER", "1") not in ("0", "", "false")
+# qubit relabelling between passes (plan_passes_remap): plan-specialised forward programs without
+# Pauli frames / checkpoints / caller states
+REMAP = __import__("os").environ.get("QF_REMAP", "1") not in ("0", "", "false")
 
 
 # ---------------------------------------------------------------------------
@@ -701,6 +790,9 @@ class Program:
     blocks: np.ndarray = None
     block_factors: np.ndarray = None
     block_gens: np.ndarray = None
+    # qubit relabelling (plan_passes_remap): physical bit of every logical qubit after the last
+    # pass (None: identity layout)
+    final_pos: list = None
 
 
 def _bit_subset(mask: int, reg_glob: list) -> int:
@@ -883,7 +975,28 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     if not adjoint:
         for oid in obs_diag_ids:
             obs_ops.append(Op(OP_OBS, tuple(range(n)), obs=oid))
-    passes = plan_passes(ops, n, L)
+    if frame and REMAP and jit and not adjoint and not mirror and not from_state and n > L:
+        # a Pauli frame only pays off through normalised rotations; a program whose dense ops
+        # would all absorb it (brickwork / RCS) is relabelled instead
+        def _normalisable(o):
+            if o.kind == OP_DENSE1:
+                axes = {infos[gi].axis for gi in o.factors}
+                return len(axes) == 1 and axes <= {"X", "Y"}
+            return (o.kind == OP_DENSE2 and len(o.factors) == 1 and infos[o.factors[0]].symbolic
+                    and bool(infos[o.factors[0]].pstring))
+        if not any(_normalisable(o) for o in ops):
+            frame = False
+    remap = (REMAP and jit and not adjoint and not mirror and not from_state and not frame and n > L)
+    passes = plan_passes_remap(ops, n, L) if remap else plan_passes(ops, n, L)
+    if remap and all(p.out_pos == [p.pos_in[q] for q in p.qubits] for p in passes):
+        remap = False                          # nothing moved: the plain layout
+        for p in passes:
+            p.pos_in = p.out_pos = None
+    final_pos = list(range(n))
+    if remap:
+        final_pos = list(passes[-1].pos_in)
+        for q, o in zip(passes[-1].qubits, passes[-1].out_pos):
+            final_pos[q] = o
     for p in passes:
         plan_stages(p, R)
     if obs_ops:
@@ -931,9 +1044,21 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         prow[14] = len(em.term_mask)
         prow[80] = len(em.grp)
         prow[82] = len(em.op_rows)
-        outer = [q for q in range(n) if q not in set(p.qubits)]
+        posi = p.pos_in if p.pos_in is not None else list(range(n))   # logical -> physical at load
+
+        def phys_mask(m, posi=posi):
+            out = 0
+            for q in range(n):
+                if m >> q & 1:
+                    out |= 1 << posi[q]
+            return out
+
+        outer = sorted(posi[q] for q in range(n) if q not in set(p.qubits))
         prow[10] = len(outer)
         prow[16:16 + len(outer)] = outer
+        if p.out_pos is not None:
+            prow[84:84 + len(p.out_pos)] = p.out_pos
+            prow[126] = 1
         prow[48:80] = -1
         if not adjoint and first_fwd:
             for q, op in sorted(init.items()):
@@ -949,13 +1074,14 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         for si, st in enumerate(stages):
             regs, thr = stage_slots(p, st, R, edge=st is p.stages[0] or st is p.stages[-1])
             srow = np.zeros(STAGE_INTS, dtype=np.int32)
-            reg_glob = [p.qubits[b] for b in regs]
+            reg_log = [p.qubits[b] for b in regs]
+            reg_glob = [posi[q] for q in reg_log]          # physical positions
             srow[0:R] = reg_glob
-            srow[8:8 + len(thr)] = [p.qubits[b] for b in thr]
+            srow[8:8 + len(thr)] = [posi[p.qubits[b]] for b in thr]
             srow[24:24 + R] = [swizzle(1 << b) for b in regs]
             srow[32:32 + len(thr)] = [swizzle(1 << b) for b in thr]
             srow[48] = len(em.op_rows)
-            slot_of = {q: j for j, q in enumerate(reg_glob)}
+            slot_of = {q: j for j, q in enumerate(reg_log)}
             st_ops = list(reversed(st.ops)) if adjoint else list(st.ops)
             if adjoint and lam_diag and last_fwd and si == 0:
                 st_ops = obs_ops + st_ops
@@ -1042,7 +1168,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                             ev[7] = int(orow[14])                  # merged slot: 1 head, 2 member
                         events.append(ev)
                 elif op.kind == OP_DIAG:
-                    terms = em.diag_terms(op)
+                    terms = [(phys_mask(m), i_, w_) for m, i_, w_ in em.diag_terms(op)]
                     b_, e_, g_ = em.emit_terms(terms, reg_glob)
                     orow[4], orow[5], orow[6] = b_, e_, g_
                     if adjoint and op.symbolic:
@@ -1057,7 +1183,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                     for ti, t in enumerate(obs.terms):
                         xm, zm, ny = term_masks(t)
                         assert xm == 0
-                        terms.append((zm, -1 - em.n_coef, 0.0))  # negative: coefficient column
+                        terms.append((phys_mask(zm), -1 - em.n_coef, 0.0))  # negative: coefficient column
                         em.coef_cols.append((op.obs, ti))
                         em.n_coef += 1
                     b_, e_, g_ = em.emit_terms(terms, reg_glob)
@@ -1137,7 +1263,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         dense_fbeg=np.array(fbeg, dtype=np.int32), factor=np.array(flat, dtype=np.int32),
         term_src=tsrc.reshape(-1), term_beta=tbeta,
     )
-    stats = dict(passes=len(passes), stages=len(em.stage_rows), ops=len(em.op_rows),
+    stats = dict(passes=len(passes), stages=len(em.stage_rows), ops=len(em.op_rows), remapped=bool(remap),
                  stages_per_pass=[len(p.stages) for p in passes],
                  ops_per_pass=[len(p.ops) for p in passes], product_init=len(init),
                  tile_qubits=[p.qubits for p in passes])
@@ -1158,6 +1284,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         blocks=np.array(blocks, dtype=np.int32).reshape(-1, 4),
         block_factors=np.array(bfac, dtype=np.int32).reshape(-1, 3),
         block_gens=np.array(bgen, dtype=np.float64),
+        final_pos=final_pos if remap else None,
     )
 
 

@@ -137,7 +137,32 @@ def run_forward(prog: pl.Program, mats, angs, B, n, coefs=None, init_state=None)
                         for k in range(o[4], o[5]):
                             h += coefs[-1 - prog.term_idx[k]] * _chi(idx, prog.term_mask[k])
                         slots[b, o[7]] += float(np.sum(np.abs(psi[b]) ** 2 * h))
+            if p[126]:      # relabelled store: tile bit at physical tileq[i] goes to p[84 + i]
+                outer = set(int(x) for x in p[16:16 + p[10]])
+                tileq = [q for q in range(n) if q not in outer]
+                psi[b] = permute_bits(psi[b], {tileq[i]: int(p[84 + i]) for i in range(len(tileq))}, n)
     return psi, slots
+
+
+def permute_bits(v, perm: dict, n: int):
+    """out[j] = v[i] where bit perm[a] of j is bit a of i (bits not in perm stay)."""
+    idx = np.arange(1 << n)
+    j = idx.copy()
+    for a, b in perm.items():
+        j &= ~(1 << b)
+    for a, b in perm.items():
+        j |= ((idx >> a) & 1) << b
+    out = np.empty_like(v)
+    out[j] = v
+    return out
+
+
+def logical_state(psi, prog: pl.Program, n: int):
+    """A relabelled program's output in the logical layout (physical bit final_pos[q] = qubit q)."""
+    if prog.final_pos is None:
+        return psi
+    inv = {prog.final_pos[q]: q for q in range(n)}
+    return np.stack([permute_bits(row, inv, n) for row in psi])
 
 
 def run_adjoint(prog: pl.Program, mats, angs, B, n, psi, lam, hcoefs):

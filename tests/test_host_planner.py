@@ -217,3 +217,25 @@ def test_block_fused_adjoint_random_circuits_emulated(seed, n):
     if not any(o.symbolic and len(o.factors) > 1 for o in pl.build_ops(pl.analyse(circ, si), True, block=True)):
         pytest.skip("no block formed")
     _check_program(circ, random_observable(rng, n, diag=True), max(n, pl.N_MIN), theta, block=True)
+
+
+@pytest.mark.parametrize("n,depth,seed", [(16, 8, 3), (20, 6, 5)])
+def test_relabelled_passes_emulated_vs_oracle(n, depth, seed):
+    """planner.plan_passes_remap (plan-specialised forward programs): each pass stores its tile
+    permuted so the next pass's qubits sit on the lane bits; fewer passes than the fixed
+    layout, the same state (logical layout via Program.final_pos) and the same sum-Z value."""
+    circ = wl.brickwork_circuit(n, depth, seed)
+    infos = pl.analyse(circ, {})
+    zs = wl.z_sum(n)
+    plain = pl.build_program(circ, pl.analyse(circ, {}), n, adjoint=False, observables=[zs], obs_diag_ids=[0])
+    prog = pl.build_program(circ, infos, n, adjoint=False, observables=[zs], obs_diag_ids=[0], jit=True)
+    assert prog.stats["remapped"] and prog.final_pos is not None
+    assert len(prog.passes) < len(plain.passes), (len(prog.passes), len(plain.passes))
+    em.check_invariants(prog)
+    fixed, consts = pl.concrete_tables([circ], infos)
+    mats, angs = em.build_tables(prog, np.zeros((1, 0)), fixed, consts)
+    psi, slots = em.run_forward(prog, mats, angs, 1, n, np.ones(n))
+    ref = orc.simulate_amps(circ, {})
+    np.testing.assert_allclose(em.logical_state(psi, prog, n)[0], ref, atol=1e-12)
+    E = em.slots_to_cols(slots, prog.obs_slots, 1)[0, 0]
+    assert E == pytest.approx(orc.expectation(ref, zs, n), abs=1e-10)
