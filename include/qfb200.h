@@ -238,6 +238,11 @@ int qf_sample(const float* psi, int n, int rows, int shots, const uint64_t* keys
 int qf_sample_multi(const float* psi, int n, int rows, int keys_per_row, int shots, const uint64_t* keys,
                     double* scratch, int64_t* out_idx, int32_t* near_boundary, void* stream);
 
+/* State of a relabelled program (planner.plan_passes_remap: qubit q on physical bit pos[q],
+ * host array [n]) back to the logical layout: out[row, j] = in[row, i], bit pos[q] of i = bit q
+ * of j.  The StateVector the reference's simulate returns (qcflow/sim.py:139-150) is logical. */
+int qf_permute_bits(const float* in, float* out, int n, int rows, const int32_t* pos, void* stream);
+
 /* ---- plan-specialised kernels (jit.py generates CUDA source from the descriptors above) ---- */
 
 /* NVRTC-compile `src` (libnvrtc.so.12 loaded at run time) into a cubin; free with qf_jit_free. */

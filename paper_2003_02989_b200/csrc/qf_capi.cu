@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 
@@ -915,6 +916,40 @@ int qf_sample_multi(const float* psi, int n, int rows, int keys_per_row, int sho
   draw_kernel<<<(unsigned)((dw * 32 + 255) / 256), 256, 0, s>>>(p, n, rows, keys_per_row, shots, keys, prefix,
                                                                out_idx, near_boundary);
   return check_launch("draw_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// Relabelled programs (planner.plan_passes_remap) leave qubit q on physical bit pos[q]:
+// out[row, j] = in[row, i] with bit pos[q] of i = bit q of j.  Writes are coalesced.
+// ---------------------------------------------------------------------------
+struct BitMap { int32_t pos[32]; };
+
+__global__ void permute_bits_kernel(const float2* __restrict__ in, float2* __restrict__ out, int n, int64_t total,
+                                    BitMap m) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = g >> n;
+    const uint64_t j = (uint64_t)g & ((1ull << n) - 1);
+    uint64_t i = 0;
+#pragma unroll 8
+    for (int q = 0; q < n; ++q) i |= ((j >> q) & 1ull) << m.pos[q];
+    out[g] = in[(row << n) | (int64_t)i];
+  }
+}
+
+int qf_permute_bits(const float* in, float* out, int n, int rows, const int32_t* pos, void* stream) {
+  if (rows == 0) return 0;
+  if (n < 1 || n > 32) {
+    set_error("qf_permute_bits: n=%d outside [1, 32]", n);
+    return 2;
+  }
+  BitMap m{};
+  for (int q = 0; q < n; ++q) m.pos[q] = pos[q];
+  const int64_t total = (int64_t)rows << n;
+  const int T = 256;
+  const int64_t blocks = std::min<int64_t>((total + T - 1) / T, 148LL * 64);
+  permute_bits_kernel<<<(unsigned)blocks, T, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float2*>(in), reinterpret_cast<float2*>(out), n, total, m);
+  return check_launch("permute_bits_kernel");
 }
 
 int qf_sample(const float* psi, int n, int rows, int shots, const uint64_t* keys, double* scratch, int64_t* out_idx,

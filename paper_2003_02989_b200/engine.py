@@ -539,11 +539,14 @@ def _obs_key(o) -> tuple:
 
 
 def _unrelabel(psi: torch.Tensor, final_pos, n: int) -> torch.Tensor:
-    """[B, 2^n] state whose physical bit final_pos[q] is logical qubit q -> logical layout."""
-    B = psi.shape[0]
-    v = psi.reshape([B] + [2] * n)                 # dim 1 + (n - 1 - b) holds physical bit b
-    dims = [0] + [1 + (n - 1 - final_pos[n - 1 - d]) for d in range(n)]
-    return v.permute(dims).contiguous().reshape(B, 1 << n)
+    """[B, 2^n] state whose physical bit final_pos[q] is logical qubit q -> logical layout
+    (one coalesced-write gather kernel, ``qf_permute_bits``)."""
+    lib = nat.load()
+    out = torch.empty_like(psi)
+    pos = (C.c_int32 * n)(*[int(x) for x in final_pos])
+    nat.check(lib.qf_permute_bits(_ptr(psi), _ptr(out), n, psi.shape[0], C.cast(pos, C.c_void_p),
+                                  torch.cuda.current_stream(psi.device).cuda_stream))
+    return out
 
 
 class Engine:

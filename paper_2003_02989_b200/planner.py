@@ -717,13 +717,23 @@ def plan_stages(p: Pass, R: int) -> None:
             raise AssertionError("stage planner made no progress")
     if not stages:
         stages.append(Stage(list(range(L - R, L)), []))
-    # store needs lanes on local bits 0..4
-    if min(stages[-1].regs) < LANE_Q:
-        stages.append(Stage(list(range(L - R, L)), []))
+    # the store needs lanes on the local bits stored to physical 0..3: local 0..3, or for a
+    # relabelled pass the bits whose out_pos < 4 (then the load and store stages differ)
+    sl = store_lanes(p)
+    if set(stages[-1].regs) & set(sl) or (len(stages) == 1 and sl != list(range(LANE_Q))):
+        free = [b for b in range(L - 1, -1, -1) if b not in sl]
+        stages.append(Stage(sorted(free[:R]), []))
     p.stages = stages
 
 
-def stage_slots(p: Pass, st: Stage, R: int, edge: bool = True):
+def store_lanes(p: Pass) -> list:
+    """Local bits the pass stores to physical bits 0..LANE_Q-1, in that order."""
+    if p.out_pos is None:
+        return list(range(LANE_Q))
+    return [p.out_pos.index(k) for k in range(LANE_Q)]
+
+
+def stage_slots(p: Pass, st: Stage, R: int, edge: bool = True, lanes: list = None):
     """(register local bits, thread local bits [lanes first]).
 
     Edge stages (a pass's first / last, which load / store global memory) keep the lowest
@@ -734,6 +744,8 @@ def stage_slots(p: Pass, st: Stage, R: int, edge: bool = True):
     L = len(p.qubits)
     rs = set(st.regs)
     free = [b for b in range(L) if b not in rs]
+    if lanes is not None:     # a relabelled pass's store stage: its store lanes first
+        return list(st.regs), list(lanes) + [b for b in free if b not in lanes]
     if edge or CONFLICT_FREE_LANES is False:
         return list(st.regs), free
     lanes, seen = [], set()
@@ -1072,7 +1084,8 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         # frame walk next to tau), so the slot needs one store and one reduction per tile
         merge_heads: dict = {}
         for si, st in enumerate(stages):
-            regs, thr = stage_slots(p, st, R, edge=st is p.stages[0] or st is p.stages[-1])
+            regs, thr = stage_slots(p, st, R, edge=st is p.stages[0] or st is p.stages[-1],
+                                    lanes=store_lanes(p) if (p.out_pos is not None and st is p.stages[-1]) else None)
             srow = np.zeros(STAGE_INTS, dtype=np.int32)
             reg_log = [p.qubits[b] for b in regs]
             reg_glob = [posi[q] for q in reg_log]          # physical positions

@@ -89,8 +89,16 @@ def check_invariants(prog: pl.Program):
             st = prog.stages[si]
             reg_glob = list(st[0:R])
             lanes = list(st[8:12])
-            if si == sb or si == se - 1:
+            if si == sb:
                 assert lanes == [0, 1, 2, 3], (si, lanes)
+            if si == se - 1:
+                if p[126]:   # relabelled: the store lanes are the bits stored to physical 0..3
+                    outer = set(int(x) for x in p[16:16 + p[10]])
+                    tileq = [q for q in range(prog.n) if q not in outer]
+                    out_of = {tileq[i]: int(p[84 + i]) for i in range(len(tileq))}
+                    assert [out_of[int(x)] for x in lanes] == [0, 1, 2, 3], (si, lanes)
+                else:
+                    assert lanes == [0, 1, 2, 3], (si, lanes)
             for o in prog.ops[st[48]:st[49]]:
                 if o[0] == pl.OP_DENSE2:
                     assert 0 <= o[1] < o[2] < R
