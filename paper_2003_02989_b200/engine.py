@@ -563,7 +563,7 @@ class Engine:
         overrides = overrides or {}
         topo = pl.topology_key(template, symbol_index)
         key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state, frame,
-               tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block, jit)
+               tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block, jit, pl.REMAP)
         with self._lock:
             hit = self._plans.get(key)
             if hit is not None:
@@ -627,7 +627,7 @@ class Engine:
         uniform = _uniform(circuits)
         ckey = ("uniform", id(circuits.circuit), len(circuits)) if uniform else tuple(map(id, circuits))
         key = (ckey, symbol_names, tuple(_obs_key(o) for o in observables), bool(want_grad), str(dev),
-               bool(from_state), bool(want_state), bool(norm_identity), pl.FUSION_ENABLED)
+               bool(from_state), bool(want_state), bool(norm_identity), pl.FUSION_ENABLED, pl.REMAP)
         with self._lock:
             hit = self._bound.get(key)
             if hit is not None:

@@ -760,8 +760,11 @@ def stage_slots(p: Pass, st: Stage, R: int, edge: bool = True, lanes: list = Non
 
 CONFLICT_FREE_LANES = __import__("os").environ.get("QF_LANE_ORDER", "1") not in ("0", "", "false")
 # qubit relabelling between passes (plan_passes_remap): plan-specialised forward programs without
-# Pauli frames / checkpoints / caller states
-REMAP = __import__("os").environ.get("QF_REMAP", "1") not in ("0", "", "false")
+# Pauli frames / checkpoints / caller states.  Measured: cfg5 26 -> 16 passes but 620 -> 601 ms,
+# cfg4 22 -> 14 passes but 162 -> 186 ms -- dense brickwork passes are FMA-bound (217 fused
+# blocks x 8 FFMA2 per amplitude = 0.40 s floor at 32 qubits), so fewer HBM passes buy little
+# and the extra store stages cost more; off by default
+REMAP = __import__("os").environ.get("QF_REMAP", "0") not in ("0", "", "false")
 
 
 # ---------------------------------------------------------------------------

@@ -255,3 +255,29 @@ def test_cli_matches_reference_cli(cuda, tmp_path, monkeypatch):
             assert [x[0] for x in gl] == [x[0] for x in wl_]
             tol = 2e-3 if "central" in run["argv"] else 2e-6 + GABS
             np.testing.assert_allclose([float(x[1]) for x in gl], [float(x[1]) for x in wl_], atol=tol)
+
+
+def test_relabelled_programs_match_fixed_layout(cuda, monkeypatch):
+    """planner.plan_passes_remap on the GPU (QF_REMAP, off by default): relabelled stores,
+    expectation from physical-position masks, states brought back by qf_permute_bits -- equal
+    to the fixed-layout run and to the oracle."""
+    import torch
+
+    from paper_2003_02989_b200 import planner as pl
+
+    circ = wl.brickwork_circuit(20, 8, 11)
+    th = torch.zeros((4, 0), device="cuda")
+    obs = [wl.z_sum(20)]
+    st0 = ops.state([circ] * 4, [], th)
+    e0 = ops.expectation([circ] * 4, [], th, obs)
+    monkeypatch.setattr(pl, "REMAP", True)
+    from paper_2003_02989_b200.engine import ENGINE
+
+    b = ENGINE.bind([circ] * 4, [], obs, want_state=True)
+    assert b.plan.fwd.prog.final_pos is not None            # the relabelled program is in use
+    st1 = ops.state([circ] * 4, [], th)
+    e1 = ops.expectation([circ] * 4, [], th, obs)
+    torch.testing.assert_close(st1, st0, atol=2e-6, rtol=0)
+    torch.testing.assert_close(e1, e0, atol=1e-5, rtol=0)
+    ref = orc.simulate_amps(circ, {})
+    np.testing.assert_allclose(st1[0].cpu().numpy(), ref, atol=AMP)

@@ -220,13 +220,14 @@ def test_block_fused_adjoint_random_circuits_emulated(seed, n):
 
 
 @pytest.mark.parametrize("n,depth,seed", [(16, 8, 3), (20, 6, 5)])
-def test_relabelled_passes_emulated_vs_oracle(n, depth, seed):
+def test_relabelled_passes_emulated_vs_oracle(n, depth, seed, monkeypatch):
     """planner.plan_passes_remap (plan-specialised forward programs): each pass stores its tile
     permuted so the next pass's qubits sit on the lane bits; fewer passes than the fixed
     layout, the same state (logical layout via Program.final_pos) and the same sum-Z value."""
     circ = wl.brickwork_circuit(n, depth, seed)
     infos = pl.analyse(circ, {})
     zs = wl.z_sum(n)
+    monkeypatch.setattr(pl, "REMAP", True)
     plain = pl.build_program(circ, pl.analyse(circ, {}), n, adjoint=False, observables=[zs], obs_diag_ids=[0])
     prog = pl.build_program(circ, infos, n, adjoint=False, observables=[zs], obs_diag_ids=[0], jit=True)
     assert prog.stats["remapped"] and prog.final_pos is not None
