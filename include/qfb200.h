@@ -243,6 +243,16 @@ int qf_sample_multi(const float* psi, int n, int rows, int keys_per_row, int sho
  * of j.  The StateVector the reference's simulate returns (qcflow/sim.py:139-150) is logical. */
 int qf_permute_bits(const float* in, float* out, int n, int rows, const int32_t* pos, void* stream);
 
+/* ---- tensor-core dense blocks (prototype, csrc/qf_tc.cu) ----
+ * A 16 x 16 complex unitary on qubits 0..3 of a [rows, 2^n] complex64 state (n in [11, 32]) on
+ * the tcgen05 tensor cores: kind::tf32 MMAs (M=128, N=32, K=32 in real form) with 3xTF32 error
+ * compensation, TMEM accumulators.  The gate-apply of sim.apply_matrix (qcflow/sim.py:88-105)
+ * for a dense 4-qubit block.  qf_dense4_tc_prepare (host) builds the B operand image
+ * [2][32][32] floats (tf32 hi, lo parts) from U as (re, im) doubles, row-major; the caller
+ * copies it to the device.  in == out is allowed. */
+int qf_dense4_tc_prepare(const double* u, float* out);
+int qf_dense4_tc(const float* in, float* out, int n, int rows, const float* bmat, void* stream);
+
 /* ---- plan-specialised kernels (jit.py generates CUDA source from the descriptors above) ---- */
 
 /* NVRTC-compile `src` (libnvrtc.so.12 loaded at run time) into a cubin; free with qf_jit_free. */

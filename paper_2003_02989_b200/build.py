@@ -9,7 +9,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["qf_pass.cu", "qf_capi.cu", "qf_jit.cu"]
+SOURCES = ["qf_pass.cu", "qf_capi.cu", "qf_jit.cu", "qf_tc.cu"]
 LIB = os.path.join(HERE, "libqfb200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

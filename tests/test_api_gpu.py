@@ -281,3 +281,25 @@ def test_relabelled_programs_match_fixed_layout(cuda, monkeypatch):
     torch.testing.assert_close(e1, e0, atol=1e-5, rtol=0)
     ref = orc.simulate_amps(circ, {})
     np.testing.assert_allclose(st1[0].cpu().numpy(), ref, atol=AMP)
+
+
+def test_dense4_tensor_core_block_matches_fp64(cuda):
+    """csrc/qf_tc.cu: a 16 x 16 unitary on qubits 0..3 through tcgen05 kind::tf32 MMAs with
+    3xTF32 compensation equals the fp64 product to complex64 accuracy (1e-6 of the amplitude
+    scale), out of place and in place."""
+    import torch
+
+    from paper_2003_02989_b200 import tensorcore as tc
+
+    rng = np.random.default_rng(21)
+    q, _ = np.linalg.qr(rng.normal(size=(16, 16)) + 1j * rng.normal(size=(16, 16)))
+    rows, n = 8, 16
+    a = rng.normal(size=(rows, 1 << n)) + 1j * rng.normal(size=(rows, 1 << n))
+    a /= np.linalg.norm(a, axis=1, keepdims=True)
+    psi = torch.as_tensor(a.astype(np.complex64)).cuda()
+    ref = (a.astype(np.complex64).astype(np.complex128).reshape(rows, -1, 16) @ q.T).reshape(rows, -1)
+    out = tc.apply_dense4(psi, q)
+    scale = np.abs(ref).max()
+    assert np.abs(out.cpu().numpy() - ref).max() < 1e-6 * scale
+    tc.apply_dense4(psi, q, out=psi)                     # in place
+    assert np.abs(psi.cpu().numpy() - ref).max() < 1e-6 * scale
