@@ -160,7 +160,12 @@ def _run(circuits, symbol_names, vals, observables=(), *, want_grad=False, want_
                     v = vals if idx is None else vals[torch.as_tensor(idx, device=vals.device)]
                     up = None
                     if upstream is not None:
-                        up = upstream if idx is None else np.asarray(upstream)[idx]
+                        if idx is None:
+                            up = upstream
+                        elif isinstance(upstream, torch.Tensor):
+                            up = upstream[torch.as_tensor(idx, device=upstream.device)]
+                        else:
+                            up = np.asarray(upstream)[idx]
                     out = bound.execute(_to_dev(v, d), upstream=up, want_grad=want_grad, want_state=want_state,
                                         want_expect=want_expect)
                     if post is not None:
