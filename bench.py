@@ -382,44 +382,58 @@ def run_gpu(args, rank, world):
              f"adjoint L{ad.prog.L}/R{ad.prog.R}, Pauli-frame normalised={bool(fw.frame)}, "
              f"checkpointed adjoint={ckpt is not None})"
              if jf is not None else "qf::pass_kernel (interpreted)")
+    # the launch sequence execute() issues: forward passes, the turn kernel (forward's last
+    # pass + backward's first in one launch, jit.TurnKernel) when the plan has one, backward passes
+    turn = bound._turn() if ck else None
+    amps = (1 << n_eff) * B
+
+    def f_launch(p):
+        if ck:
+            jf.run_ckpt(B, ck, [0] + ck[:-1], 0, _ptr(mats_f), _ptr(angs_f), _ptr(bound.fwd_coefs), 0,
+                        _ptr(part_f), s, False, which=[p])
+        elif jf is not None:
+            jf.run(B, _ptr(psi), 0, _ptr(mats_f), _ptr(angs_f), _ptr(bound.fwd_coefs), 0, _ptr(part_f), s,
+                   first=p, last=p + 1)
+        else:
+            nat.check(lib.qf_run_passes(C.byref(fw.struct), p, p + 1, _ptr(psi), n_eff, B, _ptr(mats_f),
+                                        _ptr(angs_f), _ptr(bound.fwd_coefs), _ptr(part_f), fw.tiles, s))
+
+    def a_launch(p):
+        if ck:
+            ja.run_ckpt(B, ck[::-1], None, _ptr(lam), _ptr(mats_a), _ptr(angs_a), _ptr(hw), hw.shape[1],
+                        _ptr(part_a), s, True, which=[p])
+        elif ja is not None:
+            ja.run(B, _ptr(psi), _ptr(lam), _ptr(mats_a), _ptr(angs_a), _ptr(hw), hw.shape[1], _ptr(part_a), s,
+                   first=p, last=p + 1)
+        else:
+            nat.check(lib.qf_adjoint_passes(C.byref(struct_a), p, p + 1, _ptr(psi), _ptr(lam), n_eff, B,
+                                            _ptr(mats_a), _ptr(angs_a), _ptr(hw), _ptr(part_a), ad.tiles, s))
+
+    launches = [(f"qf_f_p{p}", fb[p], (lambda p=p: f_launch(p))) for p in range(len(fb) - (1 if turn else 0))]
+    if turn is not None:
+        # reads psi (checkpoint P-2) and writes lambda: 16 B per amplitude
+        launches.append(("qf_turn", 16 * amps, lambda: turn.run(
+            B, ck[len(fb) - 2], _ptr(mats_f), _ptr(angs_f), _ptr(bound.fwd_coefs), _ptr(part_f), _ptr(lam),
+            _ptr(mats_a), _ptr(angs_a), _ptr(hw), hw.shape[1], _ptr(part_a), s)))
+    launches += [(f"qf_a_p{p}", ab[p], (lambda p=p: a_launch(p))) for p in range(1 if turn else 0, len(ab))]
     reps = 5
-    samp_f, samp_a = [], []
+    samp = []
     for r in range(reps + 1):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(fb) + len(ab) + 1)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(launches) + 1)]
         ev[0].record(stream)
-        for p in range(len(fb)):
-            if ck:
-                jf.run_ckpt(B, ck, [0] + ck[:-1], 0, _ptr(mats_f), _ptr(angs_f), _ptr(bound.fwd_coefs), 0,
-                            _ptr(part_f), s, False, which=[p])
-            elif jf is not None:
-                jf.run(B, _ptr(psi), 0, _ptr(mats_f), _ptr(angs_f), _ptr(bound.fwd_coefs), 0, _ptr(part_f), s,
-                       first=p, last=p + 1)
-            else:
-                nat.check(lib.qf_run_passes(C.byref(fw.struct), p, p + 1, _ptr(psi), n_eff, B, _ptr(mats_f),
-                                            _ptr(angs_f), _ptr(bound.fwd_coefs), _ptr(part_f), fw.tiles, s))
-            ev[1 + p].record(stream)
-        for p in range(len(ab)):
-            if ck:
-                ja.run_ckpt(B, ck[::-1], None, _ptr(lam), _ptr(mats_a), _ptr(angs_a), _ptr(hw), hw.shape[1],
-                            _ptr(part_a), s, True, which=[p])
-            elif ja is not None:
-                ja.run(B, _ptr(psi), _ptr(lam), _ptr(mats_a), _ptr(angs_a), _ptr(hw), hw.shape[1], _ptr(part_a), s,
-                       first=p, last=p + 1)
-            else:
-                nat.check(lib.qf_adjoint_passes(C.byref(struct_a), p, p + 1, _ptr(psi), _ptr(lam), n_eff, B,
-                                                _ptr(mats_a), _ptr(angs_a), _ptr(hw), _ptr(part_a), ad.tiles, s))
-            ev[1 + len(fb) + p].record(stream)
+        for i, (_, _, fn) in enumerate(launches):
+            fn()
+            ev[1 + i].record(stream)
         torch.cuda.synchronize(dev)
         if r == 0:
             continue  # warm-up round
-        samp_f.append([ev[p].elapsed_time(ev[p + 1]) for p in range(len(fb))])
-        samp_a.append([ev[len(fb) + p].elapsed_time(ev[len(fb) + p + 1]) for p in range(len(ab))])
-    # per-pass median over the repetitions (a single hiccup must not skew the roofline)
-    times_f = np.median(np.array(samp_f), axis=0)
-    times_a = np.median(np.array(samp_a), axis=0)
+        samp.append([ev[i].elapsed_time(ev[i + 1]) for i in range(len(launches))])
+    # per-launch median over the repetitions (a single hiccup must not skew the roofline)
+    times = np.median(np.array(samp), axis=0)
     peak, peak_kind = _peaks()
-    tot_bytes = sum(fb) + sum(ab)
-    tot_ms = times_f.sum() + times_a.sum()
+    byts = [b_ for _, b_, _ in launches]
+    tot_bytes = sum(byts)
+    tot_ms = float(times.sum())
     achieved = tot_bytes / (tot_ms / 1000.0) / 1e9
     # DRAM traffic cannot be read in-run (no ncu inside a timed bench): it comes from the
     # committed ncu capture of this same command, labelled with its source
@@ -479,7 +493,7 @@ def run_gpu(args, rank, world):
         # per step: passes + 2 builds (qf_build_ops: dense + angle kernels each) + 2 frame
         # walks + 3 slot reductions (expectation, gradient, energy); no ATen kernels remain in
         # the step (cross-checked against the ncu launch list under profiles/)
-        launches = len(fb) + len(ab) + 4 + (2 if fw.frame else 0) + 3
+        n_launch = len(launches) + 4 + (2 if fw.frame else 0) + 3
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -488,8 +502,8 @@ def run_gpu(args, rank, world):
                        "per_gpu_batch": BATCH, "n_qubits": N_QUBITS, "depth": DEPTH,
                        "observable": "sum_E ZZ (30 edges)", "gradient": "adjoint",
                        "parallelism": f"batch-shard x{world}", "l2": "inputs exceed L2 (2 GiB state per GPU)",
-                       "fwd_passes": len(fb), "adj_passes": len(ab)},
-            "gpu_launches": launches * args.steps,
+                       "fwd_passes": len(fb), "adj_passes": len(ab), "turn_kernel": turn is not None},
+            "gpu_launches": n_launch * args.steps,
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(theta_np.nbytes),
                     "d2h_bytes_per_step": int(BATCH * (1 + len(syms)) * 8)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
@@ -497,9 +511,9 @@ def run_gpu(args, rank, world):
                          "traffic_source": traffic_src,
                          "kernel": kname,
                          "algorithmic_bytes_per_step": tot_bytes, "kernel_ms_per_step": tot_ms,
-                         "pass_ms": [round(x, 4) for x in list(times_f) + list(times_a)],
-                         "pass_gbs": [round(b / (t / 1000) / 1e9, 1) for b, t in
-                                      zip(list(fb) + list(ab), list(times_f) + list(times_a))]},
+                         "pass_names": [nm for nm, _, _ in launches],
+                         "pass_ms": [round(float(x), 4) for x in times],
+                         "pass_gbs": [round(b_ / (t / 1000) / 1e9, 1) for b_, t in zip(byts, times)]},
             "clocks": clocks,
             "cpu_baseline": cpu,
             "gpu_parameter_shift": ps,

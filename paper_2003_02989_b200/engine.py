@@ -391,7 +391,22 @@ class Bound:
         partials = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
         # relabelled programs exist only as plan-specialised kernels
         jf = fw.jit(dev, B, force=remote is not None or fw.prog.final_pos is not None)
-        if ckpt:
+        turn = self._turn() if ckpt else None
+        prep = None
+        if ckpt and turn is not None:
+            # forward passes 0..P-2, then ONE kernel for the forward's last pass and the
+            # backward's first (the final state stays in registers), then backward 1..P-1
+            ck = ckpt[0]
+            P = len(ck)
+            prep = self._adjoint_prep(lib, psi, theta, upstream, stream, frame_f, ckpt)
+            jf.run_ckpt(B, [_ptr(t) for t in ck], [0] + [_ptr(t) for t in ck[:-1]], 0, _ptr(mats), _ptr(angs),
+                        _ptr(self.fwd_coefs), 0, _ptr(partials), stream, False, which=range(P - 1))
+            hw_t = prep["hw_t"]
+            turn.run(B, _ptr(ck[P - 2]), _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), _ptr(partials),
+                     _ptr(prep["lam"]), _ptr(prep["mats"]), _ptr(prep["angs"]), _ptr(hw_t), hw_t.shape[1],
+                     _ptr(prep["partials"]), stream)
+            self._adjoint_launch(lib, prep, psi, stream, ckpt, first=1)
+        elif ckpt:
             ck = ckpt[0]
             jf.run_ckpt(B, [_ptr(t) for t in ck], [0] + [_ptr(t) for t in ck[:-1]], 0, _ptr(mats), _ptr(angs),
                         _ptr(self.fwd_coefs), 0, _ptr(partials), stream, False)
@@ -429,7 +444,10 @@ class Bound:
             st = psi[:, : (1 << plan.n)]
             out["state"] = st.clone() if want_grad else st
         if want_grad:
-            self._adjoint(lib, psi, theta, upstream, stream, out, frame_f, ckpt)
+            if prep is not None:      # the turn kernel already ran the backward sweep
+                self._adjoint_reduce(lib, prep, stream, out)
+            else:
+                self._adjoint(lib, psi, theta, upstream, stream, out, frame_f, ckpt)
         return out
 
     def _checkpoints(self, psi, wanted):
@@ -455,6 +473,13 @@ class Bound:
         return ck, torch.empty((self.B, P), dtype=torch.float64, device=self.device)
 
     def _adjoint(self, lib, psi, theta, upstream, stream, out, frame_f=None, ckpt=None):
+        prep = self._adjoint_prep(lib, psi, theta, upstream, stream, frame_f, ckpt)
+        self._adjoint_launch(lib, prep, psi, stream, ckpt, first=0)
+        self._adjoint_reduce(lib, prep, stream, out)
+
+    def _adjoint_prep(self, lib, psi, theta, upstream, stream, frame_f=None, ckpt=None) -> dict:
+        """Per-call tables of the backward sweep: Hamiltonian weights, built matrices / angles,
+        the frame walk, lambda and the slot partials."""
         plan, dev, B = self.plan, self.device, self.B
         ad = plan.adj
         n_eff = plan.n_eff
@@ -480,20 +505,28 @@ class Bound:
                                              _ptr(angs), ad.prog.n_ang, _ptr(scale), ad.prog.n_slots, _ptr(frame_f),
                                              None, pm[0], pm[1], ad.n_stage, stream))
         lam = torch.empty_like(psi)
-        if not self.lam_diag:
+        partials = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
+        return dict(hw_t=hw_t, mats=mats, angs=angs, scale=scale, lam=lam, partials=partials)
+
+    def _adjoint_launch(self, lib, prep, psi, stream, ckpt, first=0):
+        """The backward pass kernels from pass ``first`` (1 after the turn kernel)."""
+        plan, dev, B = self.plan, self.device, self.B
+        ad = plan.adj
+        n_eff = plan.n_eff
+        hw_t, mats, angs, lam, partials = prep["hw_t"], prep["mats"], prep["angs"], prep["lam"], prep["partials"]
+        if not self.lam_diag and first == 0:
             if self.hkeys:
                 xm, zm, ny = self.h_arrays
                 nat.check(lib.qf_pauli_apply(_ptr(psi), _ptr(lam), n_eff, B, len(self.hkeys), _ptr(xm), _ptr(zm),
                                              _ptr(ny), _ptr(hw_t), hw_t.shape[1], stream))
             else:
                 lam.zero_()
-        partials = torch.empty((B, max(ad.prog.n_slots, 1), ad.tiles), dtype=torch.float64, device=dev)
         # block-fused and R = 5 adjoint programs exist only as plan-specialised kernels
         ja = ad.jit(dev, B, force=ad.n_blocks > 0 or ad.prog.R != pl.ADJ_R)
         if ckpt:
             ck = ckpt[0]
             ja.run_ckpt(B, [_ptr(t) for t in reversed(ck)], None, _ptr(lam), _ptr(mats), _ptr(angs), _ptr(hw_t),
-                        hw_t.shape[1], _ptr(partials), stream, True)
+                        hw_t.shape[1], _ptr(partials), stream, True, which=range(first, len(ck)))
         elif ja is not None:
             ja.run(B, _ptr(psi), _ptr(lam), _ptr(mats), _ptr(angs), _ptr(hw_t), hw_t.shape[1], _ptr(partials),
                    stream)
@@ -503,6 +536,11 @@ class Bound:
             nat.check(lib.qf_adjoint_passes(C.byref(struct), 0, len(ad.prog.passes), _ptr(psi), _ptr(lam), n_eff,
                                             B, _ptr(mats), _ptr(angs), _ptr(hw_t), _ptr(partials), ad.tiles,
                                             stream))
+
+    def _adjoint_reduce(self, lib, prep, stream, out):
+        plan, dev, B = self.plan, self.device, self.B
+        ad = plan.adj
+        mats, partials, scale = prep["mats"], prep["partials"], prep["scale"]
         # every column is written by the first reduction (S > 0)
         grad = torch.empty((B, self.S), dtype=torch.float64, device=dev) if self.S else \
             torch.zeros((B, 1), dtype=torch.float64, device=dev)
@@ -529,6 +567,22 @@ class Bound:
                                                  1, _ptr(energy), 0, _ptr(scale), stream))
             out["energy"] = energy[:, 0]
         out["grad"] = grad[:, : self.S]
+
+    def _turn(self):
+        """The turn kernel (jit.TurnKernel: forward's last pass + backward's first pass in one
+        launch) for this plan, or None."""
+        plan = self.plan
+        if os.environ.get("QF_TURN", "1") in ("0", "", "false") or plan.adj is None:
+            return None
+        if "turn" not in plan.extra:
+            from . import jit as _jit
+
+            with _JIT_LOCK:
+                if "turn" not in plan.extra:
+                    ok = _jit._turn_compatible(plan.fwd.prog, plan.adj.prog)
+                    plan.extra["turn"] = _jit.TurnKernel(plan.fwd.prog, plan.adj.prog,
+                                                         self.device.index or 0) if ok else None
+        return plan.extra["turn"]
 
 
 def _obs_key(o) -> tuple:

@@ -184,12 +184,16 @@ def _block_code(D: int, mhi: int, mlo: int, slot_rel: int, gs_store, indent: str
     return lines
 
 
-def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 0) -> tuple[list, list, list]:
+def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 0, fuse: str = None,
+             only_pass: int = None) -> tuple[list, list, list]:
     """Per-pass CUDA kernel sources (without prelude), kernel names, launch geometry.
 
     ``remote_pass``: that pass stores into the receive shards of the other ranks instead of
     in place (a global-qubit swap fused into the pass, distributed.py): amplitude ``idx`` of
-    rank s goes to rank idx >> (n - g) at (idx & low) | (s << (n - g))."""
+    rank s goes to rank idx >> (n - g) at (idx & low) | (s << (n - g)).
+    ``fuse`` / ``only_pass``: one pass as a part of the turn kernel (``generate_turn``):
+    "head" leaves the tile in v0 instead of storing it, "tail" starts from v0 instead of
+    loading it."""
     n, L, R, adj = prog.n, prog.L, prog.R, prog.adjoint
     TB = L - R
     NR, NT = 1 << R, 1 << TB
@@ -205,6 +209,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
     names, geo = [], []
     for pi, p in enumerate(prog.passes):
         if remote_pass >= 0 and pi != remote_pass:
+            continue
+        if only_pass is not None and pi != only_pass:
             continue
         name = f"qf_{tag}_p{pi}" + ("_rs" if pi == remote_pass else "")
         names.append(name)
@@ -429,7 +435,13 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         mark_load = len(o)
         st0 = st_rows[0]
         w(f"  const u32 gt0 = base | {_xor_expr(tglob(st0))};")
-        if prefetch:
+        if fuse == "tail":
+            # the turn kernel's backward part: psi is already in registers (the forward part's
+            # last stage layout, exchanged to this pass's first stage by generate_turn)
+            if adj:
+                for r in range(NR):
+                    w(f"  v1[{r}] = make_float2(0.f, 0.f);")
+        elif prefetch:
             # this tile landed in PF (natural local order) during the previous tile
             def lidx(qs):
                 return [1 << tileq.index(q) for q in qs]
@@ -851,7 +863,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             w("  }")
 
         # ---- store ----
-        if store:
+        if store and fuse != "head":
             stl = st_rows[-1]
             if int(p[126]):
                 # relabelled pass (planner.plan_passes_remap): tile bit at physical position
@@ -921,6 +933,113 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         w("}")
         src.append("\n".join(o) + "\n")
     return src, names, geo
+
+
+def _turn_compatible(fwd: pl.Program, adj: pl.Program) -> bool:
+    """The turn kernel joins the forward's last pass and the backward's first pass: both
+    programs must be checkpoint mirrors with the same tile geometry."""
+    if not (adj.adjoint and not fwd.adjoint and fwd.L == adj.L and fwd.R == adj.R and fwd.n == adj.n):
+        return False
+    P = len(fwd.passes)
+    if P != len(adj.passes) or P < 2:
+        return False
+    pf, pa = fwd.passes[P - 1], adj.passes[0]
+    outer_f = sorted(int(x) for x in pf[16:16 + int(pf[10])])
+    outer_a = sorted(int(x) for x in pa[16:16 + int(pa[10])])
+    return outer_f == outer_a and int(pa[2]) == pl.INIT_LOAD_PSI and not int(pf[126])
+
+
+def generate_turn(fwd: pl.Program, adj: pl.Program, name: str = "qf_turn") -> tuple[str, int, int]:
+    """One kernel for the forward's last tile pass and the backward's first (checkpointed,
+    lambda = H psi fused): the final state never leaves registers -- no store of it by the
+    forward, no load of it by the backward.  Parameters (forward args ``a``, backward args
+    ``b``).  Returns (source, threads per CTA, dynamic smem bytes)."""
+    P = len(fwd.passes)
+    fs, _, fg = generate(fwd, "f", fuse="head", only_pass=P - 1)
+    bs, _, bg = generate(adj, "a", fuse="tail", only_pass=0)
+    NT, NR = fg[0][0], 1 << fwd.R
+    assert bg[0][0] == NT
+    import re
+
+    def body(src):
+        lines = src.rstrip("\n").split("\n")
+        head = lines[0]
+        m = re.search(r"__launch_bounds__\((\d+), (\d+)\)", head)
+        keep = [ln for ln in lines[1:-1] if ln not in (
+            "  extern __shared__ __align__(16) unsigned char smem_raw[];",
+            f"  float2 v0[{NR}];", f"  float2 v1[{NR}];")]
+        return keep, int(m.group(2))
+
+    fb, mf = body(fs[0])
+    ab, ma = body(bs[0])
+    ab = [re.sub(r"\ba\.", "b.", ln) for ln in ab]
+    o = [f'extern "C" __global__ void __launch_bounds__({NT}, {min(mf, ma)}) {name}(const QfJitArgs a, '
+         f'const QfJitArgs b) {{',
+         "  extern __shared__ __align__(16) unsigned char smem_raw[];",
+         f"  float2 v0[{NR}];", f"  float2 v1[{NR}];", "  {"] + fb + ["  }", "  __syncthreads();"]
+    # forward's last stage layout -> backward's first stage layout (if they differ)
+    R, TB = fwd.R, fwd.L - fwd.R
+    sf = fwd.stages[int(fwd.passes[P - 1][1]) - 1]
+    sa = adj.stages[int(adj.passes[0][0])]
+    same = all(int(sf[j]) == int(sa[j]) for j in range(R)) and all(int(sf[8 + i]) == int(sa[8 + i]) for i in range(TB))
+    if not same:
+        def tp(st):
+            return _xor_expr([int(st[32 + i]) for i in range(TB)])
+
+        def ro(st, r):
+            x = 0
+            for j in range(R):
+                if r >> j & 1:
+                    x ^= int(st[24 + j])
+            return x
+        o.append("  { float2* sm = reinterpret_cast<float2*>(smem_raw); const u32 t = threadIdx.x;")
+        o.append(f"    {{ const u32 tp = {tp(sf)};")
+        o += [f"      sm[tp ^ {ro(sf, r)}u] = v0[{r}];" for r in range(NR)]
+        o.append("    }")
+        o.append("    __syncthreads();")
+        o.append(f"    {{ const u32 tp = {tp(sa)};")
+        o += [f"      v0[{r}] = sm[tp ^ {ro(sa, r)}u];" for r in range(NR)]
+        o.append("    }")
+        o.append("    __syncthreads();")
+        o.append("  }")
+    o += ["  {"] + ab + ["  }", "}"]
+    return "\n".join(o) + "\n", NT, max(fg[0][1], bg[0][1])
+
+
+class QfTurnArgs(C.Structure):
+    _fields_ = [("a", QfJitArgs), ("b", QfJitArgs)]
+
+
+class TurnKernel:
+    """The compiled turn kernel of one (forward, backward) program pair."""
+
+    def __init__(self, fwd: pl.Program, adj: pl.Program, device_index: int):
+        lib = nat.load()
+        src, self.nt, self.smem = generate_turn(fwd, adj)
+        img = compile_kernel(src, "qf_turn")
+        self.module = C.c_void_p()
+        nat.check(lib.qf_jit_load(img, C.byref(self.module)))
+        f = C.c_void_p()
+        nat.check(lib.qf_jit_function(self.module, b"qf_turn", max(self.smem, 48 * 1024), C.byref(f)))
+        self.func = (C.c_void_p * 1)(f.value)
+        self.fwd, self.adj = fwd, adj
+        self.rows_shift = fwd.n - fwd.L
+
+    def run(self, rows, psi_src, mats_f, angles_f, coefs_f, partials_f, lam, mats_a, angles_a, coefs_a,
+            coef_stride_a, partials_a, stream):
+        lib = nat.load()
+        f, a = self.fwd, self.adj
+        args = QfTurnArgs(
+            a=QfJitArgs(psi=psi_src, lam=0, mats=mats_f, angles=angles_f, coefs=coefs_f, partials=partials_f,
+                        n_mat=f.n_mat, n_ang=f.n_ang, coef_stride=0, n_slots=f.n_slots, tiles_log2=self.rows_shift,
+                        pad=rows, psi_src=psi_src, skip_psi=0),
+            b=QfJitArgs(psi=psi_src, lam=lam, mats=mats_a, angles=angles_a, coefs=coefs_a, partials=partials_a,
+                        n_mat=a.n_mat, n_ang=a.n_ang, coef_stride=coef_stride_a, n_slots=a.n_slots,
+                        tiles_log2=self.rows_shift, pad=rows, psi_src=0, skip_psi=1))
+        grid = (C.c_uint32 * 1)(rows << self.rows_shift)
+        block = (C.c_uint32 * 1)(self.nt)
+        smem = (C.c_uint32 * 1)(self.smem)
+        nat.check(lib.qf_jit_run(self.func, grid, block, smem, 1, stream, C.byref(args), C.sizeof(args)))
 
 
 _OPTS = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", b"--device-as-default-execution-space"]
