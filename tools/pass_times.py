@@ -43,6 +43,18 @@ def run_ckpt(self, *a, which=None):
 
 
 J.JitProgram.run, J.JitProgram.run_ckpt = run, run_ckpt
+_turn_run = J.TurnKernel.run
+
+
+def turn_run(self, *a, **k):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _turn_run(self, *a, **k)
+    e1.record()
+    REC.append(("t", 0, e0, e1))
+
+
+J.TurnKernel.run = turn_run
 
 
 def bound_for(cfg):
@@ -79,9 +91,12 @@ def main():
         torch.cuda.synchronize()
         for kind, p, e0, e1 in REC:
             samples.setdefault((kind, p), []).append(e0.elapsed_time(e1))
-    fw = [round(float(np.median(samples[("f", p)])), 4) for p in range(len(b.plan.fwd.prog.passes))]
-    ad = [round(float(np.median(samples[("a", p)])), 4) for p in range(len(b.plan.adj.prog.passes))]
-    print(json.dumps({"config": cfg, "fwd_ms": fw, "adj_ms": ad, "fwd_total": round(sum(fw), 3),
+    fw = [round(float(np.median(samples[("f", p)])), 4) for p in range(len(b.plan.fwd.prog.passes))
+          if ("f", p) in samples]
+    ad = [round(float(np.median(samples[("a", p)])), 4) for p in range(len(b.plan.adj.prog.passes))
+          if ("a", p) in samples]
+    turn = round(float(np.median(samples[("t", 0)])), 4) if ("t", 0) in samples else None
+    print(json.dumps({"config": cfg, "fwd_ms": fw, "adj_ms": ad, "turn_ms": turn, "fwd_total": round(sum(fw), 3),
                       "adj_total": round(sum(ad), 3), "ckpt": bool(b.plan.extra.get("ckpt")),
                       "geometry": [b.plan.fwd.prog.L, b.plan.fwd.prog.R, b.plan.adj.prog.L, b.plan.adj.prog.R]}))
 
