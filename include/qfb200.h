@@ -253,6 +253,14 @@ int qf_permute_bits(const float* in, float* out, int n, int rows, const int32_t*
 int qf_dense4_tc_prepare(const double* u, float* out);
 int qf_dense4_tc(const float* in, float* out, int n, int rows, const float* bmat, void* stream);
 
+/* Tensor-core stages of a forward program (planner tc_blocks): per (row, block) the 16 x 16
+ * product of the stage's dense ops from the row's matrix slab, as the MMA B image (tf32 hi, lo).
+ * ops [n_ops, 4] = (kind 1 = 2x2 / 2 = 4x4, matrix offset, slot 0, slot 1), bptr [n_blocks+1],
+ * out [rows, n_blocks, 2048] floats.  Part of run_ops / fusion (qcflow/sim.py:122-136,
+ * fusion.py:78-176): the products the tile passes apply with tcgen05 MMAs. */
+int qf_tc_build(const float* mats, int n_mat, int rows, const int32_t* ops, const int32_t* bptr, int n_blocks,
+                float* out, void* stream);
+
 /* ---- plan-specialised kernels (jit.py generates CUDA source from the descriptors above) ---- */
 
 /* NVRTC-compile `src` (libnvrtc.so.12 loaded at run time) into a cubin; free with qf_jit_free. */

@@ -19,6 +19,7 @@ EXPORTS = (
     "qf_jit_compile", "qf_jit_free", "qf_jit_load", "qf_jit_function", "qf_jit_unload", "qf_jit_run",
     "qf_reduce_slots_scaled", "qf_frame_walk", "qf_jit_occupancy", "qf_frame_walk_ckpt", "qf_block_grads",
     "qf_sample_multi", "qf_reduce_slots_offset", "qf_permute_bits", "qf_dense4_tc_prepare", "qf_dense4_tc",
+    "qf_tc_build",
 )
 
 _p = C.c_void_p
@@ -88,6 +89,7 @@ def load(build_if_missing: bool = True):
     lib.qf_permute_bits.argtypes = [_p, _p, C.c_int, C.c_int, _p, _p]
     lib.qf_dense4_tc_prepare.argtypes = [_p, _p]
     lib.qf_dense4_tc.argtypes = [_p, _p, C.c_int, C.c_int, _p, _p]
+    lib.qf_tc_build.argtypes = [_p, C.c_int, C.c_int, _p, _p, C.c_int, _p, _p]
     lib.qf_sample_multi.argtypes = [_p, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p, _p, _p, _p]
     lib.qf_reduce_slots_offset.argtypes = [_p, C.c_int, C.c_int, C.c_int, _p, _p, C.c_int, _p, C.c_int, _p, _p,
                                            _p]

@@ -175,9 +175,97 @@ __global__ void __launch_bounds__(128) dense4_tc_kernel(const float4* __restrict
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
 }
 
+// Tensor-core stages of the tile-pass kernels (planner tc_blocks, jit.py): per (row, block) the
+// 16 x 16 product of the stage's dense ops (matrices from the row's slab, applied on register
+// slots exactly as apply1m / apply2m do), written as the MMA's B image: [2][32][32] floats, B^T
+// rows n = 2i + c of K = 2j + d, tf32 hi then lo.  One warp per (row, block); lane c < 16 carries
+// column c of the product in fp64.
+__global__ void tc_build_kernel(const float2* __restrict__ mats, int n_mat, int rows, const int32_t* __restrict__ ops,
+                                const int32_t* __restrict__ bptr, int n_blocks, float* __restrict__ out) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= (int64_t)rows * n_blocks) return;
+  const int row = (int)(warp / n_blocks), blk = (int)(warp % n_blocks);
+  const int c = lane & 15;
+  double cr[16], ci[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    cr[r] = r == c ? 1.0 : 0.0;
+    ci[r] = 0.0;
+  }
+  const float2* M = mats + (size_t)row * n_mat;
+  for (int k = bptr[blk]; k < bptr[blk + 1]; ++k) {
+    const int kind = ops[4 * k], moff = ops[4 * k + 1], s0 = ops[4 * k + 2], s1 = ops[4 * k + 3];
+    if (kind == 1) {   // 2 x 2 on slot s0
+      const float2 m00 = M[moff], m01 = M[moff + 1], m10 = M[moff + 2], m11 = M[moff + 3];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (r & (1 << s0)) continue;
+        const int r1 = r | (1 << s0);
+        const double ar = cr[r], ai = ci[r], br = cr[r1], bi = ci[r1];
+        cr[r] = m00.x * ar - m00.y * ai + m01.x * br - m01.y * bi;
+        ci[r] = m00.x * ai + m00.y * ar + m01.x * bi + m01.y * br;
+        cr[r1] = m10.x * ar - m10.y * ai + m11.x * br - m11.y * bi;
+        ci[r1] = m10.x * ai + m10.y * ar + m11.x * bi + m11.y * br;
+      }
+    } else {           // 4 x 4 on slots (s0 msb, s1 lsb)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if (r & ((1 << s0) | (1 << s1))) continue;
+        const int idx[4] = {r, r | (1 << s1), r | (1 << s0), r | (1 << s0) | (1 << s1)};
+        double xr[4], xi[4];
+        for (int j = 0; j < 4; ++j) {
+          xr[j] = cr[idx[j]];
+          xi[j] = ci[idx[j]];
+        }
+        for (int i = 0; i < 4; ++i) {
+          double yr = 0.0, yi = 0.0;
+          for (int j = 0; j < 4; ++j) {
+            const float2 m = M[moff + i * 4 + j];
+            yr += m.x * xr[j] - m.y * xi[j];
+            yi += m.x * xi[j] + m.y * xr[j];
+          }
+          cr[idx[i]] = yr;
+          ci[idx[i]] = yi;
+        }
+      }
+    }
+  }
+  if (lane >= 16) return;
+  // column c of U: U[i][c] = (cr[i], ci[i]);  B^T[n = 2i + cc][k = 2c + d]
+  float* O = out + ((size_t)row * n_blocks + blk) * 2048;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const double vals[4] = {cr[i], -ci[i], ci[i], cr[i]};   // (cc, d) = (0,0), (0,1), (1,0), (1,1)
+    for (int q = 0; q < 4; ++q) {
+      const int n = 2 * i + (q >> 1), k = 2 * c + (q & 1);
+      const float f = (float)vals[q];
+      const float hi = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
+      O[n * 32 + k] = hi;
+      O[1024 + n * 32 + k] = (float)(vals[q] - (double)hi);
+    }
+  }
+}
+
 }  // namespace qf
 
 extern "C" {
+
+// The B images of a program's tensor-core stages: ops [n_ops, 4] = (kind 1/2, matrix offset,
+// slot 0, slot 1) in application order, bptr [n_blocks + 1]; out [rows, n_blocks, 2048] floats.
+int qf_tc_build(const float* mats, int n_mat, int rows, const int32_t* ops, const int32_t* bptr, int n_blocks,
+                float* out, void* stream) {
+  if (rows == 0 || n_blocks == 0) return 0;
+  const int64_t warps = (int64_t)rows * n_blocks;
+  qf::tc_build_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const float2*>(mats), n_mat, rows, ops, bptr, n_blocks, out);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    qf::set_error("tc_build_kernel launch: %s", cudaGetErrorString(e));
+    return 1;
+  }
+  return 0;
+}
 
 // Host: the B operand image of a 16 x 16 complex U (row-major (re, im) doubles), split into
 // tf32 hi and lo parts: out[2][32][32] floats, B^T rows (n) of K = 32.

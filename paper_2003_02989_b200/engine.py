@@ -104,6 +104,16 @@ class DeviceProgram:
         span = [int(e[3]) + (16 if int(e[0]) in (pl.EV_ABS2, pl.EV_NP) else 4)
                 for e in ev if int(e[0]) in (pl.EV_NX, pl.EV_NY, pl.EV_ABS1, pl.EV_ABS2, pl.EV_NP)]
         self.n_stage = min(max(span, default=1), max(prog.n_mat, 1))
+        # tensor-core stages: recipe of every block's 16 x 16 product (qf_tc_build)
+        self.n_tc = len(prog.tc_blocks or [])
+        if self.n_tc:
+            flat, ptr_ = [], [0]
+            for blk_ in prog.tc_blocks:
+                for kind_, moff_, s0_, s1_ in blk_:
+                    flat.append((1 if kind_ == pl.OP_DENSE1 else 2, moff_, s0_, s1_))
+                ptr_.append(len(flat))
+            self.t_tc_ops = up(np.array(flat, dtype=np.int32).reshape(-1), torch.int32)
+            self.t_tc_ptr = up(np.array(ptr_, dtype=np.int32), torch.int32)
         # block-fused adjoint: A slots reduced into consecutive columns, one range per block
         blk = prog.blocks if prog.blocks is not None else np.zeros((0, 4), np.int32)
         self.n_blocks = int(blk.shape[0])
@@ -389,8 +399,15 @@ class Bound:
         else:
             frame_f = None
         partials = torch.empty((B, max(fw.prog.n_slots, 1), fw.tiles), dtype=torch.float64, device=dev)
-        # relabelled programs exist only as plan-specialised kernels
-        jf = fw.jit(dev, B, force=remote is not None or fw.prog.final_pos is not None)
+        # relabelled programs and tensor-core stages exist only as plan-specialised kernels; the
+        # stages' B images are built from the (frame-walked) slab
+        jf = fw.jit(dev, B, force=remote is not None or fw.prog.final_pos is not None or fw.n_tc > 0)
+        tcb = None
+        if fw.n_tc:
+            tcb = torch.empty((B, fw.n_tc, 2048), dtype=torch.float32, device=dev)
+            nat.check(lib.qf_tc_build(_ptr(mats), fw.prog.n_mat, B, _ptr(fw.t_tc_ops), _ptr(fw.t_tc_ptr), fw.n_tc,
+                                      _ptr(tcb), stream))
+        tck = dict(tcb=_ptr(tcb), tc_n=fw.n_tc)
         turn = self._turn() if ckpt else None
         prep = None
         if ckpt and turn is not None:
@@ -400,7 +417,7 @@ class Bound:
             P = len(ck)
             prep = self._adjoint_prep(lib, psi, theta, upstream, stream, frame_f, ckpt)
             jf.run_ckpt(B, [_ptr(t) for t in ck], [0] + [_ptr(t) for t in ck[:-1]], 0, _ptr(mats), _ptr(angs),
-                        _ptr(self.fwd_coefs), 0, _ptr(partials), stream, False, which=range(P - 1))
+                        _ptr(self.fwd_coefs), 0, _ptr(partials), stream, False, which=range(P - 1), **tck)
             hw_t = prep["hw_t"]
             turn.run(B, _ptr(ck[P - 2]), _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), _ptr(partials),
                      _ptr(prep["lam"]), _ptr(prep["mats"]), _ptr(prep["angs"]), _ptr(hw_t), hw_t.shape[1],
@@ -409,10 +426,10 @@ class Bound:
         elif ckpt:
             ck = ckpt[0]
             jf.run_ckpt(B, [_ptr(t) for t in ck], [0] + [_ptr(t) for t in ck[:-1]], 0, _ptr(mats), _ptr(angs),
-                        _ptr(self.fwd_coefs), 0, _ptr(partials), stream, False)
+                        _ptr(self.fwd_coefs), 0, _ptr(partials), stream, False, **tck)
         elif jf is not None:
             jf.run(B, _ptr(psi), 0, _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), 0, _ptr(partials), stream,
-                   remote=remote)
+                   remote=remote, **tck)
         else:
             nat.check(lib.qf_run_passes(C.byref(fw.struct), 0, len(fw.prog.passes), _ptr(psi), n_eff, B,
                                         _ptr(mats), _ptr(angs), _ptr(self.fwd_coefs), _ptr(partials), fw.tiles,

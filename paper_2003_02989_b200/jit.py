@@ -42,7 +42,8 @@ class QfJitArgs(C.Structure):
                 ("coefs", C.c_void_p), ("partials", C.c_void_p), ("n_mat", C.c_int), ("n_ang", C.c_int),
                 ("coef_stride", C.c_int), ("n_slots", C.c_int), ("tiles_log2", C.c_int), ("pad", C.c_int),
                 ("peers", C.c_void_p), ("rank_base", C.c_int), ("pad2", C.c_int),
-                ("psi_src", C.c_void_p), ("skip_psi", C.c_int), ("pad3", C.c_int)]
+                ("psi_src", C.c_void_p), ("skip_psi", C.c_int), ("pad3", C.c_int),
+                ("tcb", C.c_void_p), ("tc_n", C.c_int), ("pad4", C.c_int)]
 
 
 FUSED_GRAD = os.environ.get("QF_FUSED_GRAD", "0") not in ("0", "", "false")   # measured 2% slower
@@ -268,6 +269,13 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         NPF = (2 if (adj and init == pl.INIT_LOAD) else 1) if prefetch else 0
         pf_off = smem
         smem += NPF * TILE * 8
+        # tensor-core stages (planner tc_blocks): A reuses the exchange tile (16 KB at offset 0,
+        # 1024-aligned), then A_lo (16 KB), the B image (8 KB), an mbarrier and the TMEM slot
+        tc_stages = [s_ for s_ in range(sb, se) if int(prog.stages[s_][50])] if not adj else []
+        if tc_stages:
+            assert NT == 128 and NR == 16 and TILE * 8 == 16384, (NT, NR, TILE)
+            tc_off = (smem + 1023) // 1024 * 1024
+            smem = tc_off + 16384 + 8192 + 64
         tileq = [q for q in range(n) if q not in set(outer)]
 
         def dep(l):
@@ -315,7 +323,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         o = []
         w = o.append
         w(f'extern "C" __global__ void __launch_bounds__({NT}, {minb_p}) {name}(const QfJitArgs a) {{')
-        w("  extern __shared__ __align__(16) unsigned char smem_raw[];")
+        w(f"  extern __shared__ __align__({1024 if tc_stages else 16}) unsigned char smem_raw[];")
         w("  float2* sm = reinterpret_cast<float2*>(smem_raw);")
         # staged matrices: one 16-byte entry {Re, Im, -Im, Im} per element, so a dense apply
         # reads the broadcast real part and the (-Im, Im) pair with one LDS.128
@@ -331,6 +339,19 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         if prefetch:
             w(f"  float2* PF = reinterpret_cast<float2*>(smem_raw + {pf_off});")
         w("  const u32 t = threadIdx.x;")
+        if tc_stages:
+            w(f"  unsigned char* TCAL = smem_raw + {tc_off};")
+            w("  unsigned char* TCB = TCAL + 16384;")
+            w("  u64* TCM = reinterpret_cast<u64*>(TCB + 8192);")
+            w("  u32* TCS = reinterpret_cast<u32*>(TCM + 1);")
+            w('  if ((t >> 5) == 0) { asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;"'
+              ' :: "r"(tc_smem(TCS))); asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;"); }')
+            w('  if (t == 0) { asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(tc_smem(TCM)));'
+              ' asm volatile("fence.mbarrier_init.release.cluster;"); }')
+            w('  asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads();'
+              ' asm volatile("tcgen05.fence::after_thread_sync;");')
+            w("  const u32 tmem = *TCS;")
+            w("  u32 tcph = 0u;")
         for sl in sorted(merged_last):
             w(f"  float gm{sl} = 0.f;")
         if PERSIST:
@@ -540,7 +561,33 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 w(f"  {{ const u32 gt = base | {_xor_expr(tglob(st))};")
             else:
                 w("  {")
-            for k in (range(int(st[48]), int(st[49])) if EXP_MODE != "nocompute" else []):
+            if int(st[50]) and not adj:
+                blk = int(st[50]) - 1
+                w(f"    // tensor-core stage: the product of this stage's {int(st[49]) - int(st[48])} dense ops, "
+                  f"one 16 x 16 unitary (tc block {blk})")
+                w(f"    {{ const float4* __restrict__ tsrc = reinterpret_cast<const float4*>(a.tcb + ((size_t)row * "
+                  f"a.tc_n + {blk}) * 2048);")
+                w("      for (u32 i = t; i < 512u; i += 128u) { const u32 wh = i >> 8, nn = (i >> 3) & 31u, cc = i & 7u;"
+                  " *reinterpret_cast<float4*>(TCB + wh * 4096u + tc_swz(nn, cc)) = tsrc[i]; }")
+                w("    }")
+                w("    __syncthreads();   // the exchange's reads of the tile are done: A reuses it")
+                w("    #pragma unroll")
+                w("    for (u32 c = 0; c < 8u; ++c) {")
+                w("      const float4 x = make_float4(v0[2 * c].x, v0[2 * c].y, v0[2 * c + 1].x, v0[2 * c + 1].y);")
+                w("      *reinterpret_cast<float4*>(smem_raw + tc_swz(t, c)) = x;")
+                w("      *reinterpret_cast<float4*>(TCAL + tc_swz(t, c)) = make_float4(tf32_lo(x.x), tf32_lo(x.y), "
+                  "tf32_lo(x.z), tf32_lo(x.w));")
+                w("    }")
+                w('    asm volatile("fence.proxy.async.shared::cta;"); asm volatile("tcgen05.fence::before_thread_sync;");')
+                w('    __syncthreads(); asm volatile("tcgen05.fence::after_thread_sync;");')
+                w("    if (t == 0) tc_block_mma(tmem, smem_raw, TCAL, TCB, TCM);")
+                w("    tc_wait(TCM, tcph); tcph ^= 1u;")
+                w('    asm volatile("tcgen05.fence::after_thread_sync;");')
+                w("    tc_ld(tmem + (((t >> 5) * 32u) << 16), v0);")
+                w('    asm volatile("tcgen05.fence::before_thread_sync;"); __syncthreads();'
+                  ' asm volatile("tcgen05.fence::after_thread_sync;");')
+            for k in (range(int(st[48]), int(st[49])) if (EXP_MODE != "nocompute" and not (int(st[50]) and not adj))
+                      else []):
                 op = prog.ops[k]
                 kind = int(op[0])
                 if EXP_MODE == "nodiag" and kind == pl.OP_DIAG:
@@ -930,6 +977,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             if scnt:
                 w("  __syncthreads();   // slot partials are rewritten by the next tile")
             w("  }")
+        if tc_stages:
+            w('  if ((t >> 5) == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" :: "r"(tmem));')
         w("}")
         src.append("\n".join(o) + "\n")
     return src, names, geo
@@ -1136,7 +1185,7 @@ class JitProgram:
         return hit
 
     def run_ckpt(self, rows, psis, srcs, lam, mats, angles, coefs, coef_stride, partials, stream, skip_psi,
-                 which=None):
+                 which=None, tcb=0, tc_n=0):
         """One launch per pass with its own state pointers: psis[i] is pass i's state buffer,
         srcs[i] (forward) the buffer it loads from (0 = psis[i]); skip_psi: adjoint passes
         read psi from forward checkpoints and do not write it back."""
@@ -1145,7 +1194,7 @@ class JitProgram:
             args = QfJitArgs(psi=psis[i], lam=lam, mats=mats, angles=angles, coefs=coefs, partials=partials,
                              n_mat=self.prog.n_mat, n_ang=self.prog.n_ang, coef_stride=coef_stride,
                              n_slots=self.prog.n_slots, tiles_log2=self.rows_shift, pad=rows,
-                             psi_src=srcs[i] if srcs else 0, skip_psi=int(bool(skip_psi)))
+                             psi_src=srcs[i] if srcs else 0, skip_psi=int(bool(skip_psi)), tcb=tcb, tc_n=tc_n)
             total = rows << self.rows_shift
             # a per-call grid array: JitPrograms are shared across threads and batch sizes
             grid = (C.c_uint32 * 1)(min(total, self.resident[i]) if self.persist else total)
@@ -1154,20 +1203,21 @@ class JitProgram:
                                      C.addressof(self.smem) + 4 * i, 1, stream, C.byref(args), C.sizeof(args)))
 
     def run(self, rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first=0, last=None,
-            remote=None):
+            remote=None, tcb=0, tc_n=0):
         """remote = (device array of the ranks' receive-shard pointers, rank of row 0, g): the
         last pass writes its output into those shards (a fused global-qubit swap)."""
         lib = nat.load()
         last = self.n if last is None else last
         args = QfJitArgs(psi=psi, lam=lam, mats=mats, angles=angles, coefs=coefs, partials=partials,
                          n_mat=self.prog.n_mat, n_ang=self.prog.n_ang, coef_stride=coef_stride,
-                         n_slots=self.prog.n_slots, tiles_log2=self.rows_shift, pad=rows)
+                         n_slots=self.prog.n_slots, tiles_log2=self.rows_shift, pad=rows, tcb=tcb, tc_n=tc_n)
         if remote is not None:
             peers, rank_base, g = remote
             args.peers, args.rank_base = peers, rank_base
             if last == self.n:
                 if last - 1 > first:
-                    self.run(rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first, last - 1)
+                    self.run(rows, psi, lam, mats, angles, coefs, coef_stride, partials, stream, first, last - 1,
+                             tcb=tcb, tc_n=tc_n)
                 f, nt, smem = self.remote_pass(g)
                 funcs = (C.c_void_p * 1)(f)
                 grid = (C.c_uint32 * 1)(rows << self.rows_shift)

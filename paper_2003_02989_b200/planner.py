@@ -765,6 +765,10 @@ CONFLICT_FREE_LANES = __import__("os").environ.get("QF_LANE_ORDER", "1") not in 
 # blocks x 8 FFMA2 per amplitude = 0.40 s floor at 32 qubits), so fewer HBM passes buy little
 # and the extra store stages cost more; off by default
 REMAP = __import__("os").environ.get("QF_REMAP", "0") not in ("0", "", "false")
+# tensor-core stages (csrc/qf_tc.cu): forward dense programs at 16 x 128 amplitudes per tile;
+# a stage qualifies when its dense work is at least TC_MIN_FFMA2 FFMA2 per amplitude
+TC_STAGES = __import__("os").environ.get("QF_TC", "1") not in ("0", "", "false")
+TC_MIN_FFMA2 = int(__import__("os").environ.get("QF_TC_MIN", "16"))
 
 
 # ---------------------------------------------------------------------------
@@ -808,6 +812,9 @@ class Program:
     # qubit relabelling (plan_passes_remap): physical bit of every logical qubit after the last
     # pass (None: identity layout)
     final_pos: list = None
+    # tensor-core stages: per block [(op kind, matrix offset, slot 0, slot 1)] in application
+    # order; stage row [50] = block index + 1
+    tc_blocks: list = None
 
 
 def _bit_subset(mask: int, reg_glob: list) -> int:
@@ -835,6 +842,7 @@ class Emitter:
         self.energy_slots: list = []
         self.coef_cols = []       # (obs id, term index within observable)
         self.blocks = []          # (factor gate indices, order, D, first A slot)
+        self.tc_blocks = []       # tensor-core stages: [(op kind, matrix offset, slot 0, slot 1)]
 
     # -- per-row matrix slab --------------------------------------------------
     def dense_mat(self, op: Op, order: tuple) -> int:
@@ -1002,6 +1010,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         if not any(_normalisable(o) for o in ops):
             frame = False
     remap = (REMAP and jit and not adjoint and not mirror and not from_state and not frame and n > L)
+    tc_ok = TC_STAGES and jit and not adjoint and not mirror and R == 4 and L - R == 7
     passes = plan_passes_remap(ops, n, L) if remap else plan_passes(ops, n, L)
     if remap and all(p.out_pos == [p.pos_in[q] for q in p.qubits] for p in passes):
         remap = False                          # nothing moved: the plain layout
@@ -1214,6 +1223,17 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                         events.append([EV_OBS, -1, -1, -1, int(orow[7]), int(orow[11]), 0, 0])
                 em.op_rows.append(orow)
             srow[49] = len(em.op_rows)
+            # tensor-core stage (forward, 16 amplitudes x 128 threads per tile, plan-specialised):
+            # all of the stage's ops are full dense matrices on its register slots, so their product
+            # is one 16 x 16 unitary per row, applied by tcgen05 MMAs (csrc/qf_tc.cu, jit.py)
+            if tc_ok:
+                rows_ = em.op_rows[int(srow[48]):int(srow[49])]
+                dense = [r_ for r_ in rows_ if int(r_[0]) in (OP_DENSE1, OP_DENSE2)]
+                cost = sum(4 if int(r_[0]) == OP_DENSE1 else 8 for r_ in dense)
+                if (len(dense) == len(rows_) and cost >= TC_MIN_FFMA2 and
+                        all(int(r_[9]) in (CLS_GENERAL, CLS_XLIKE, CLS_REAL) for r_ in dense)):
+                    srow[50] = len(em.tc_blocks) + 1
+                    em.tc_blocks.append([(int(r_[0]), int(r_[3]), int(r_[1]), int(r_[2])) for r_ in dense])
             em.stage_rows.append(srow)
         if frame and not adjoint:
             events.append([EV_PASS, -1, -1, -1, -1, -1, fwd_index, 0])
@@ -1301,6 +1321,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         block_factors=np.array(bfac, dtype=np.int32).reshape(-1, 3),
         block_gens=np.array(bgen, dtype=np.float64),
         final_pos=final_pos if remap else None,
+        tc_blocks=em.tc_blocks or None,
     )
 
 
