@@ -10,7 +10,8 @@
 // with B[2j][2i] = Re U_ij, B[2j+1][2i] = -Im U_ij, B[2j][2i+1] = Im U_ij, B[2j+1][2i+1] =
 // Re U_ij: an M=128, N=32, K=32 GEMM per 128 rows (2048 amplitudes) read and written in place
 // of the state's own bytes.  TF32 keeps 10 mantissa bits, so D = A.B_hi + A_lo.B_hi + A.B_lo
-// (A_lo = A - tf32(A), B = B_hi + B_lo split on the host; the A_lo.B_lo term is below 2^-22):
+// (A_hi = tf32(A) and A_lo = A - A_hi written explicitly, B = B_hi + B_lo split on the host; the
+// A_lo.B_lo term is below 2^-22):
 // 12 MMAs of m128n32k8 accumulate into one 128-lane x 32-column fp32 TMEM tile.
 //
 // Per CTA (128 threads, persistent over tiles): each thread stages its row of A and A_lo into
@@ -95,7 +96,7 @@ __global__ void __launch_bounds__(128) dense4_tc_kernel(const float4* __restrict
     for (uint32_t c = 0; c < 8; ++c) nxt[c] = src[c * 128 + t];
   }
   for (; tile < n_tiles; tile += gridDim.x) {
-    // ---- stage the tile: A (raw fp32; the MMA reads its tf32 part) and A_lo ----
+    // ---- stage the tile: A_hi = tf32(A) and A_lo = A - A_hi ----
 #pragma unroll
     for (uint32_t c = 0; c < 8; ++c) {
       const float4 v = nxt[c];
@@ -105,7 +106,8 @@ __global__ void __launch_bounds__(128) dense4_tc_kernel(const float4* __restrict
       lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
       lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
       lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-      *reinterpret_cast<float4*>(A + swz(row, ch)) = v;
+      // explicit tf32 hi part (hi + lo == v exactly; the MMA's own conversion may round)
+      *reinterpret_cast<float4*>(A + swz(row, ch)) = make_float4(v.x - lo.x, v.y - lo.y, v.z - lo.z, v.w - lo.w);
       *reinterpret_cast<float4*>(Alo + swz(row, ch)) = lo;
     }
     asm volatile("fence.proxy.async.shared::cta;");   // generic-proxy stores -> async-proxy (MMA) reads

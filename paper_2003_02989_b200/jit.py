@@ -275,7 +275,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         if tc_stages:
             assert NT == 128 and NR == 16 and TILE * 8 == 16384, (NT, NR, TILE)
             tc_off = (smem + 1023) // 1024 * 1024
-            smem = tc_off + 16384 + 8192 + 64
+            smem = tc_off + 16384 + 2 * 8192 + 64       # A_lo, two B images (prefetch ring)
         tileq = [q for q in range(n) if q not in set(outer)]
 
         def dep(l):
@@ -342,7 +342,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         if tc_stages:
             w(f"  unsigned char* TCAL = smem_raw + {tc_off};")
             w("  unsigned char* TCB = TCAL + 16384;")
-            w("  u64* TCM = reinterpret_cast<u64*>(TCB + 8192);")
+            w("  u64* TCM = reinterpret_cast<u64*>(TCB + 16384);")
             w("  u32* TCS = reinterpret_cast<u32*>(TCM + 1);")
             w('  if ((t >> 5) == 0) { asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;"'
               ' :: "r"(tc_smem(TCS))); asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;"); }')
@@ -352,6 +352,17 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
               ' asm volatile("tcgen05.fence::after_thread_sync;");')
             w("  const u32 tmem = *TCS;")
             w("  u32 tcph = 0u;")
+            tc_blocks_here = [int(prog.stages[s_][50]) - 1 for s_ in tc_stages]
+
+            def tc_prefetch(j):
+                """cp.async of this pass's j-th tensor-core block's B image into ring slot j % 2."""
+                b_ = tc_blocks_here[j]
+                return (f"  {{ const float4* __restrict__ tsrc = reinterpret_cast<const float4*>(a.tcb + ((size_t)"
+                        f"(blockIdx.x >> {n - L}) * a.tc_n + {b_}) * 2048);"
+                        f" for (u32 i = t; i < 512u; i += 128u) {{ const u32 wh = i >> 8, nn = (i >> 3) & 31u, "
+                        f"cc = i & 7u; cp_async16(TCB + {(j % 2) * 8192} + wh * 4096u + tc_swz(nn, cc), tsrc + i); }}"
+                        f" cp_async_commit(); }}")
+            w(tc_prefetch(0))
         for sl in sorted(merged_last):
             w(f"  float gm{sl} = 0.f;")
         if PERSIST:
@@ -563,24 +574,26 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 w("  {")
             if int(st[50]) and not adj:
                 blk = int(st[50]) - 1
+                j_tc = tc_stages.index(sb + si)
                 w(f"    // tensor-core stage: the product of this stage's {int(st[49]) - int(st[48])} dense ops, "
-                  f"one 16 x 16 unitary (tc block {blk})")
-                w(f"    {{ const float4* __restrict__ tsrc = reinterpret_cast<const float4*>(a.tcb + ((size_t)row * "
-                  f"a.tc_n + {blk}) * 2048);")
-                w("      for (u32 i = t; i < 512u; i += 128u) { const u32 wh = i >> 8, nn = (i >> 3) & 31u, cc = i & 7u;"
-                  " *reinterpret_cast<float4*>(TCB + wh * 4096u + tc_swz(nn, cc)) = tsrc[i]; }")
-                w("    }")
-                w("    __syncthreads();   // the exchange's reads of the tile are done: A reuses it")
+                  f"one 16 x 16 unitary (tc block {blk}); its B image was prefetched into ring slot {j_tc % 2}")
+                w("    cp_async_wait_all();")
+                w("    __syncthreads();   // B landed for every thread; the exchange's reads of the tile are done")
+                if j_tc + 1 < len(tc_stages):
+                    w("  " + tc_prefetch(j_tc + 1))
                 w("    #pragma unroll")
                 w("    for (u32 c = 0; c < 8u; ++c) {")
                 w("      const float4 x = make_float4(v0[2 * c].x, v0[2 * c].y, v0[2 * c + 1].x, v0[2 * c + 1].y);")
-                w("      *reinterpret_cast<float4*>(smem_raw + tc_swz(t, c)) = x;")
-                w("      *reinterpret_cast<float4*>(TCAL + tc_swz(t, c)) = make_float4(tf32_lo(x.x), tf32_lo(x.y), "
-                  "tf32_lo(x.z), tf32_lo(x.w));")
+                w("      const float4 lo = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));")
+                w("      // explicit tf32 hi part: the MMA's own fp32 -> tf32 conversion may round, and the")
+                w("      // split must satisfy hi + lo == x exactly")
+                w("      *reinterpret_cast<float4*>(smem_raw + tc_swz(t, c)) = make_float4(x.x - lo.x, x.y - lo.y, "
+                  "x.z - lo.z, x.w - lo.w);")
+                w("      *reinterpret_cast<float4*>(TCAL + tc_swz(t, c)) = lo;")
                 w("    }")
                 w('    asm volatile("fence.proxy.async.shared::cta;"); asm volatile("tcgen05.fence::before_thread_sync;");')
                 w('    __syncthreads(); asm volatile("tcgen05.fence::after_thread_sync;");')
-                w("    if (t == 0) tc_block_mma(tmem, smem_raw, TCAL, TCB, TCM);")
+                w(f"    if (t == 0) tc_block_mma(tmem, smem_raw, TCAL, TCB + {(j_tc % 2) * 8192}, TCM);")
                 w("    tc_wait(TCM, tcph); tcph ^= 1u;")
                 w('    asm volatile("tcgen05.fence::after_thread_sync;");')
                 w("    tc_ld(tmem + (((t >> 5) * 32u) << 16), v0);")
