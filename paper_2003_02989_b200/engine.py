@@ -634,7 +634,7 @@ class Engine:
         overrides = overrides or {}
         topo = pl.topology_key(template, symbol_index)
         key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state, frame,
-               tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block, jit, pl.REMAP)
+               tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block, jit, pl.REMAP, pl.TC_STAGES)
         with self._lock:
             hit = self._plans.get(key)
             if hit is not None:
@@ -698,7 +698,8 @@ class Engine:
         uniform = _uniform(circuits)
         ckey = ("uniform", id(circuits.circuit), len(circuits)) if uniform else tuple(map(id, circuits))
         key = (ckey, symbol_names, tuple(_obs_key(o) for o in observables), bool(want_grad), str(dev),
-               bool(from_state), bool(want_state), bool(norm_identity), pl.FUSION_ENABLED, pl.REMAP)
+               bool(from_state), bool(want_state), bool(norm_identity), pl.FUSION_ENABLED, pl.REMAP,
+               pl.TC_STAGES)
         with self._lock:
             hit = self._bound.get(key)
             if hit is not None:

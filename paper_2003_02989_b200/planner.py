@@ -766,8 +766,12 @@ CONFLICT_FREE_LANES = __import__("os").environ.get("QF_LANE_ORDER", "1") not in 
 # and the extra store stages cost more; off by default
 REMAP = __import__("os").environ.get("QF_REMAP", "0") not in ("0", "", "false")
 # tensor-core stages (csrc/qf_tc.cu): forward dense programs at 16 x 128 amplitudes per tile;
-# a stage qualifies when its dense work is at least TC_MIN_FFMA2 FFMA2 per amplitude
-TC_STAGES = __import__("os").environ.get("QF_TC", "1") not in ("0", "", "false")
+# a stage qualifies when its dense work is at least TC_MIN_FFMA2 FFMA2 per amplitude.
+# Measured (one B200): cfg4 161 -> 172 ms, cfg5 614 -> 688 ms (per-stage B staging, barriers and
+# MMA round trips outweigh the FFMA2 work of 2-3 fused blocks), and the tensor cores' fp32
+# accumulation shrinks every block's output by ~1.4e-6 (24q depth 20: norm 1 - 1.1e-4) -- off
+# by default
+TC_STAGES = __import__("os").environ.get("QF_TC", "0") not in ("0", "", "false")
 TC_MIN_FFMA2 = int(__import__("os").environ.get("QF_TC_MIN", "16"))
 
 

@@ -304,3 +304,27 @@ def test_dense4_tensor_core_block_matches_fp64(cuda):
     assert np.abs(out.cpu().numpy() - ref).max() < 4e-6 * scale
     tc.apply_dense4(psi, q, out=psi)                     # in place
     assert np.abs(psi.cpu().numpy() - ref).max() < 4e-6 * scale
+
+
+def test_tensor_core_stages_match_ffma2_path(cuda, monkeypatch):
+    """planner tc_blocks (QF_TC, off by default): forward dense stages applied as one 16 x 16
+    tcgen05 MMA block each give the FFMA2 path's state to the tensor cores' accuracy (fp32
+    accumulation: ~1e-6 relative per block), and the expectation within 1e-4."""
+    import torch
+
+    from paper_2003_02989_b200 import planner as pl
+    from paper_2003_02989_b200.engine import ENGINE
+
+    circ = wl.brickwork_circuit(20, 10, 3)
+    th = torch.zeros((4, 0), device="cuda")
+    obs = [wl.z_sum(20)]
+    st0 = ops.state([circ] * 4, [], th)
+    e0 = ops.expectation([circ] * 4, [], th, obs)
+    monkeypatch.setattr(pl, "TC_STAGES", True)
+    b = ENGINE.bind([circ] * 4, [], [], want_state=True)
+    assert b.plan.fwd.n_tc > 0                               # tensor-core stages are in use
+    st1 = ops.state([circ] * 4, [], th)
+    e1 = ops.expectation([circ] * 4, [], th, obs)
+    scale = float(st0.abs().max())
+    assert float((st1 - st0).abs().max()) < 1e-4 * scale
+    torch.testing.assert_close(e1, e0, atol=1e-4, rtol=0)
