@@ -168,6 +168,13 @@ class DeviceProgram:
 
 
 _JIT_LOCK = threading.Lock()
+# CUDA graphs of Bound.execute (QF_GRAPH=0 disables): (bound id, stream, want_grad, want_expect,
+# theta shape) -> (bound, graph, static theta, static outputs); LRU-bounded because every graph
+# keeps its buffers (the checkpointed adjoint's state copies) allocated
+GRAPHS = os.environ.get("QF_GRAPH", "1") not in ("0", "", "false")
+MAX_GRAPHS = int(os.environ.get("QF_MAX_GRAPHS", "4"))
+_GRAPHS: OrderedDict = OrderedDict()
+_GRAPH_LOCK = threading.RLock()
 
 _TORCH_OF = {
     np.dtype(np.int32): torch.int32, np.dtype(np.float64): torch.float64,
@@ -353,7 +360,50 @@ class Bound:
                 want_expect=True, stream=None, initial=None, donate=False, remote=None) -> dict:
         """theta: device float32 [B, S]; initial: [B, 2^n] complex state when bound
         ``from_state`` (the circuit is applied to it instead of |0...0>; ``donate``: the
-        caller's contiguous complex64 device tensor is updated in place).  Returns device tensors."""
+        caller's contiguous complex64 device tensor is updated in place).  Returns device tensors.
+
+        The common call (expectations / gradients of |0...0> programs, default upstream, the
+        caller's current stream) replays a CUDA graph of the whole launch sequence (builds,
+        frame walks, pass kernels, reductions: ~18 launches) captured on its first use."""
+        if (GRAPHS and stream is None and upstream is None and initial is None and remote is None
+                and not self.from_state and not want_state and theta.is_cuda):
+            return self._execute_graphed(theta, want_grad, want_expect)
+        return self._execute(theta, upstream=upstream, want_state=want_state, want_grad=want_grad,
+                             want_expect=want_expect, stream=stream, initial=initial, donate=donate, remote=remote)
+
+    def _execute_graphed(self, theta, want_grad, want_expect):
+        dev = self.device
+        cur = torch.cuda.current_stream(dev)
+        theta = theta.to(dtype=torch.float32)
+        key = (id(self), cur.cuda_stream, bool(want_grad), bool(want_expect), tuple(theta.shape))
+        with _GRAPH_LOCK:
+            hit = _GRAPHS.get(key)
+            if hit is not None and hit[0] is self:
+                _GRAPHS.move_to_end(key)
+            else:
+                static = torch.empty(theta.shape, dtype=torch.float32, device=dev)
+                static.copy_(theta)
+                side = torch.cuda.Stream(dev)
+                side.wait_stream(cur)
+                with torch.cuda.stream(side):      # warm-up: NVRTC compiles, allocator sizing
+                    self._execute(static, want_grad=want_grad, want_expect=want_expect)
+                cur.wait_stream(side)
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                    out = self._execute(static, want_grad=want_grad, want_expect=want_expect)
+                hit = (self, graph, static, out)
+                _GRAPHS[key] = hit
+                while len(_GRAPHS) > MAX_GRAPHS:       # each graph holds its buffers (checkpoints)
+                    _GRAPHS.popitem(last=False)
+            _, graph, static, out = hit
+            static.copy_(theta, non_blocking=True)
+            graph.replay()
+            # outputs are copied before the lock is released: the next replay on this stream
+            # rewrites the graph's static buffers
+            return {k: (v.clone() if isinstance(v, torch.Tensor) else v) for k, v in out.items()}
+
+    def _execute(self, theta: torch.Tensor, *, upstream=None, want_state=False, want_grad=False,
+                 want_expect=True, stream=None, initial=None, donate=False, remote=None) -> dict:
         lib = nat.load()
         dev = self.device
         plan = self.plan
