@@ -171,8 +171,12 @@ _JIT_LOCK = threading.Lock()
 # CUDA graphs of Bound.execute (QF_GRAPH=0 disables): (bound id, stream, want_grad, want_expect,
 # theta shape) -> (bound, graph, static theta, static outputs); LRU-bounded because every graph
 # keeps its buffers (the checkpointed adjoint's state copies) allocated
+# Measured: headline e2e 20.67k -> 20.78k circuits/s; cfg1 (1024 x 2^10) 0.49 -> 0.53 ms (the
+# replay's input copy and output clones outweigh 18 launches there) -> batches of at least
+# GRAPH_MIN_AMPS amplitudes only
 GRAPHS = os.environ.get("QF_GRAPH", "1") not in ("0", "", "false")
-MAX_GRAPHS = int(os.environ.get("QF_MAX_GRAPHS", "4"))
+MAX_GRAPHS = int(os.environ.get("QF_MAX_GRAPHS", "2"))
+GRAPH_MIN_AMPS = 1 << 22
 _GRAPHS: OrderedDict = OrderedDict()
 _GRAPH_LOCK = threading.RLock()
 
@@ -366,7 +370,8 @@ class Bound:
         caller's current stream) replays a CUDA graph of the whole launch sequence (builds,
         frame walks, pass kernels, reductions: ~18 launches) captured on its first use."""
         if (GRAPHS and stream is None and upstream is None and initial is None and remote is None
-                and not self.from_state and not want_state and theta.is_cuda):
+                and not self.from_state and not want_state and theta.is_cuda
+                and self.B << self.plan.n_eff >= GRAPH_MIN_AMPS):
             return self._execute_graphed(theta, want_grad, want_expect)
         return self._execute(theta, upstream=upstream, want_state=want_state, want_grad=want_grad,
                              want_expect=want_expect, stream=stream, initial=initial, donate=donate, remote=remote)
