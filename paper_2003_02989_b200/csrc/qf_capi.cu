@@ -49,107 +49,78 @@ struct Recipe {
   QfBuildRecipe r;
 };
 
-__device__ void gen_matrix(const QfBuildRecipe& R, int g, double v, Z* out) {
-  const int d = R.gen_dim[g];
-  const double* ev = R.gen_eval + g * 4;
-  const Z* V = reinterpret_cast<const Z*>(R.gen_evec) + g * 16;
-  Z ph[4];
-  for (int k = 0; k < d; ++k) {
-    double s, c;
-    sincos(-v * ev[k], &s, &c);
-    ph[k] = {c, s};
-  }
-  // U = V diag(ph) V^dagger   (V stored row-major d x d within a 4x4 block)
-  for (int i = 0; i < d; ++i)
-    for (int j = 0; j < d; ++j) {
+
+// y = U x for a factor on a d-dim sub-vector: U = V diag(exp(-i v lambda)) V^dagger for a
+// generator factor (no d x d matrix is formed), or the fixed matrix (row stride 4).
+__device__ __forceinline__ void factor_apply(const QfBuildRecipe& R, int kind, int src, double v, int row, int d,
+                                             Z* x) {
+  Z y[4];
+  if (kind == 0) {
+    const double* ev = R.gen_eval + src * 4;
+    const Z* V = reinterpret_cast<const Z*>(R.gen_evec) + src * 16;
+    Z w[4];
+    for (int k = 0; k < d; ++k) {   // w = diag(ph) V^dagger x
       Z acc{0, 0};
-      for (int k = 0; k < d; ++k) {
-        Z a = V[i * 4 + k];
-        Z b = V[j * 4 + k];
-        b.y = -b.y;
-        acc = zadd(acc, zmul(zmul(a, ph[k]), b));
-      }
-      out[i * 4 + j] = acc;
+      for (int j = 0; j < d; ++j) acc = zadd(acc, zmul(Z{V[j * 4 + k].x, -V[j * 4 + k].y}, x[j]));
+      double sn, cs;
+      sincos(-v * ev[k], &sn, &cs);
+      w[k] = zmul(Z{cs, sn}, acc);
     }
+    for (int i = 0; i < d; ++i) {
+      Z acc{0, 0};
+      for (int k = 0; k < d; ++k) acc = zadd(acc, zmul(V[i * 4 + k], w[k]));
+      y[i] = acc;
+    }
+  } else {
+    const Z* F = reinterpret_cast<const Z*>(R.fixed) + ((size_t)(R.fixed_rows > 1 ? row : 0) * R.n_fixed + src) * 16;
+    for (int i = 0; i < d; ++i) {
+      Z acc{0, 0};
+      for (int j = 0; j < d; ++j) acc = zadd(acc, zmul(F[i * 4 + j], x[j]));
+      y[i] = acc;
+    }
+  }
+  for (int i = 0; i < d; ++i) x[i] = y[i];
 }
 
-__global__ void build_dense_kernel(const QfBuildRecipe R, const float* theta, int64_t tstride, int rows,
-                                   float2* mats, int n_mat) {
+// One thread per (row, op, column): column c of the op's product, applying every factor to it
+// in turn (D-fold parallel and O(d^2) per factor: no 4 x 4 temporaries in local memory).
+__global__ void build_dense_col_kernel(const QfBuildRecipe R, const float* theta, int64_t tstride, int rows,
+                                       float2* mats, int n_mat) {
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= (int64_t)rows * R.n_dense) return;
-  const int row = (int)(id / R.n_dense), op = (int)(id % R.n_dense);
+  if (id >= (int64_t)rows * R.n_dense * 4) return;
+  const int col = (int)(id & 3);
+  const int64_t ro = id >> 2;
+  const int row = (int)(ro / R.n_dense), op = (int)(ro % R.n_dense);
   const int D = R.dense_dim[op];
-  Z M[16];
-  for (int i = 0; i < 16; ++i) M[i] = {(i / 4 == i % 4 && i / 4 < D) ? 1.0 : 0.0, 0.0};
+  if (col >= D) return;
+  Z m[4];
+  for (int i = 0; i < 4; ++i) m[i] = Z{i == col ? 1.0 : 0.0, 0.0};
   for (int f = R.dense_fbeg[op]; f < R.dense_fbeg[op + 1]; ++f) {
     const int kind = R.factor[3 * f], src = R.factor[3 * f + 1], emb = R.factor[3 * f + 2];
-    Z F[16];
-    int fd;
-    if (kind == 0) {
-      const double v = R.gen_coeff[src] * (double)theta[row * tstride + R.gen_sym[src]] + R.gen_const[src];
-      gen_matrix(R, src, v, F);
-      fd = R.gen_dim[src];
-    } else {
-      const Z* fx = reinterpret_cast<const Z*>(R.fixed) + ((size_t)(R.fixed_rows > 1 ? row : 0) * R.n_fixed + src) * 16;
-      for (int i = 0; i < 16; ++i) F[i] = fx[i];
-      fd = (emb == 0 || emb == 1) ? 4 : 2;
-    }
-    (void)fd;
-    if (f != R.dense_fbeg[op] && (emb == 2 || emb == 3 || emb == 4)) {
-      // one-qubit factor: mix row pairs of M in place (no embedded 4x4 copy)
-      const int bit = emb == 2 ? 2 : 1;
-      const Z f00 = F[0], f01 = F[1], f10 = F[4], f11 = F[5];
-      for (int i0 = 0; i0 < D; ++i0) {
-        if (i0 & bit) continue;
-        const int i1 = i0 | bit;
-        for (int j = 0; j < D; ++j) {
-          const Z x = M[i0 * 4 + j], y = M[i1 * 4 + j];
-          M[i0 * 4 + j] = zadd(zmul(f00, x), zmul(f01, y));
-          M[i1 * 4 + j] = zadd(zmul(f10, x), zmul(f11, y));
-        }
+    const double v = kind == 0 ? R.gen_coeff[src] * (double)theta[row * tstride + R.gen_sym[src]] + R.gen_const[src]
+                               : 0.0;
+    if (emb == 4) {                       // one-qubit op
+      factor_apply(R, kind, src, v, row, 2, m);
+    } else if (emb == 0) {                // two-qubit factor in the op's order
+      factor_apply(R, kind, src, v, row, 4, m);
+    } else if (emb == 1) {                // two-qubit factor with swapped qubits
+      Z x[4] = {m[0], m[2], m[1], m[3]};
+      factor_apply(R, kind, src, v, row, 4, x);
+      m[0] = x[0]; m[2] = x[1]; m[1] = x[2]; m[3] = x[3];
+    } else {                              // 2: F (x) I (msb), 3: I (x) F (lsb)
+      for (int a = 0; a < 2; ++a) {
+        const int i0 = emb == 2 ? a : 2 * a, i1 = emb == 2 ? a + 2 : 2 * a + 1;
+        Z x[2] = {m[i0], m[i1]};
+        factor_apply(R, kind, src, v, row, 2, x);
+        m[i0] = x[0];
+        m[i1] = x[1];
       }
-      continue;
     }
-    // embed F into the op's D-dim local space -> G
-    Z G[16];
-    if (emb == 4) {  // 1q op, 1q factor: F stored 2x2 at stride 4 or packed? -> packed 2x2 in [0..3]
-      for (int i = 0; i < 16; ++i) G[i] = {0, 0};
-      G[0] = F[0]; G[1] = F[1]; G[4] = F[4]; G[5] = F[5];
-    } else if (emb == 0 || emb == 1) {
-      const int sg[4] = {0, 2, 1, 3};
-      for (int i = 0; i < 4; ++i)
-        for (int j = 0; j < 4; ++j) G[i * 4 + j] = emb == 0 ? F[i * 4 + j] : F[sg[i] * 4 + sg[j]];
-    } else {  // 2: F (x) I (factor on MSB slot); 3: I (x) F
-      for (int i = 0; i < 4; ++i)
-        for (int j = 0; j < 4; ++j) {
-          const int ia = i >> 1, ib = i & 1, ja = j >> 1, jb = j & 1;
-          Z val{0, 0};
-          if (emb == 2) {
-            if (ib == jb) val = F[ia * 4 + ja];
-          } else {
-            if (ia == ja) val = F[ib * 4 + jb];
-          }
-          G[i * 4 + j] = val;
-        }
-    }
-    // M = G @ M (the first factor is G itself)
-    Z N[16];
-    if (f == R.dense_fbeg[op]) {
-      for (int i = 0; i < 16; ++i) N[i] = G[i];
-    } else {
-      for (int i = 0; i < D; ++i)
-        for (int j = 0; j < D; ++j) {
-          Z acc{0, 0};
-          for (int k = 0; k < D; ++k) acc = zadd(acc, zmul(G[i * 4 + k], M[k * 4 + j]));
-          N[i * 4 + j] = acc;
-        }
-    }
-    for (int i = 0; i < 16; ++i) M[i] = N[i];
   }
   float2* out = mats + (size_t)row * n_mat + R.dense_mat[op];
-  for (int i = 0; i < D; ++i)
-    for (int j = 0; j < D; ++j) out[i * D + j] = make_float2((float)M[i * 4 + j].x, (float)M[i * 4 + j].y);
+  for (int i = 0; i < D; ++i) out[i * D + col] = make_float2((float)m[i].x, (float)m[i].y);
 }
+
 
 __global__ void build_angle_kernel(const QfBuildRecipe R, const float* theta, int64_t tstride, int rows,
                                    int32_t* angles, int n_ang) {
@@ -660,10 +631,10 @@ int qf_build_ops(const QfBuildRecipe* recipe, const float* theta, int64_t theta_
   cudaStream_t s = (cudaStream_t)stream;
   const int T = 128;
   if (recipe->n_dense > 0 && rows > 0) {
-    const int64_t tot = (int64_t)rows * recipe->n_dense;
-    build_dense_kernel<<<(unsigned)((tot + T - 1) / T), T, 0, s>>>(*recipe, theta, theta_stride, rows,
-                                                                   reinterpret_cast<float2*>(mats), n_mat);
-    if (check_launch("build_dense_kernel")) return 1;
+    const int64_t tot = (int64_t)rows * recipe->n_dense * 4;
+    build_dense_col_kernel<<<(unsigned)((tot + T - 1) / T), T, 0, s>>>(*recipe, theta, theta_stride, rows,
+                                                                       reinterpret_cast<float2*>(mats), n_mat);
+    if (check_launch("build_dense_col_kernel")) return 1;
   }
   if (recipe->n_terms > 0 && rows > 0) {
     const int64_t tot = (int64_t)rows * recipe->n_terms;
