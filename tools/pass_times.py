@@ -11,6 +11,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tools"))
 
+os.environ.setdefault("QF_GRAPH", "0")  # events around each launch; a graph replay hides them
+
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -31,15 +33,15 @@ def _timed(self, launch, p):
     REC.append(("a" if self.prog.adjoint else "f", p, e0, e1))
 
 
-def run(self, rows, *a, first=0, last=None, remote=None):
+def run(self, rows, *a, first=0, last=None, **k):
     last = self.n if last is None else last
     for p in range(first, last):
-        _timed(self, lambda: _run(self, rows, *a, first=p, last=p + 1, remote=remote), p)
+        _timed(self, lambda: _run(self, rows, *a, first=p, last=p + 1, **k), p)
 
 
-def run_ckpt(self, *a, which=None):
+def run_ckpt(self, *a, which=None, **k):
     for p in (range(self.n) if which is None else which):
-        _timed(self, lambda: _run_ckpt(self, *a, which=[p]), p)
+        _timed(self, lambda: _run_ckpt(self, *a, which=[p], **k), p)
 
 
 J.JitProgram.run, J.JitProgram.run_ckpt = run, run_ckpt
