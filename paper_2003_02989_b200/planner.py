@@ -293,6 +293,8 @@ def _diag_op_qubits(gates, infos):
 
 
 FUSION_ENABLED = True   # False: one op per gate (the reference's fuse_enabled=False cells)
+# forward programs: phase gates and 1q runs on a pair join the pair's dense 4x4 (QF_ABSORB_2Q=0: off)
+ABSORB_INTO_2Q = __import__("os").environ.get("QF_ABSORB_2Q", "1") not in ("0", "", "false")
 
 
 def build_ops(infos: list[GateInfo], adjoint: bool, block: bool = False) -> list[Op]:
@@ -332,6 +334,15 @@ def build_ops(infos: list[GateInfo], adjoint: bool, block: bool = False) -> list
             if j is not None and ops[j] is not None and ops[j].kind in (OP_DENSE1, OP_DENSE2) \
                     and set(tq) <= set(ops[j].qubits):
                 ops[j].factors.append(gi)   # j is the last op on every target: exact
+                ops[j].symbolic = True
+                continue
+        if info.diag and info.symbolic and not adjoint and ABSORB_INTO_2Q:
+            # forward: a symbolic diagonal gate right after a dense two-qubit op on its qubits
+            # costs nothing as a factor of that op (the 4x4 apply is paid anyway)
+            js = {last.get(q) for q in tq}
+            j = js.pop() if len(js) == 1 else None
+            if j is not None and ops[j] is not None and ops[j].kind == OP_DENSE2 and set(tq) <= set(ops[j].qubits):
+                ops[j].factors.append(gi)
                 ops[j].symbolic = True
                 continue
         if info.diag:
@@ -392,6 +403,29 @@ def build_ops(infos: list[GateInfo], adjoint: bool, block: bool = False) -> list
             continue
         new = Op(OP_DENSE2, (a, b), factors=[], symbolic=info.symbolic,
                  sym=info.sym if info.symbolic else -1)
+        if not adjoint and ABSORB_INTO_2Q:
+            # forward: every earlier op that lives on {a, b} alone and is not followed by an
+            # op linking a or b to another qubit joins the new 4x4 (1q runs, symbolic phase
+            # gates on a / b / the pair): later ops touching them are absorbed too, ops on
+            # other qubits commute with them
+            pair, blocked, take = {a, b}, set(), []
+            for j in range(len(ops) - 1, -1, -1):
+                op = ops[j]
+                if op is None or not (set(op.qubits) & pair):
+                    continue
+                qs = set(op.qubits)
+                ok = qs <= pair and not (qs & blocked) and (
+                    op.kind == OP_DENSE1 or (op.kind == OP_DIAG and all(infos[g].symbolic for g in op.gates)))
+                if ok:
+                    take.append(j)
+                else:
+                    blocked |= qs & pair
+                    if blocked == pair:
+                        break
+            for j in reversed(take):
+                new.factors.extend(ops[j].factors if ops[j].kind == OP_DENSE1 else ops[j].gates)
+                new.symbolic |= ops[j].symbolic
+                ops[j] = None
         # absorb trailing 1q dense ops on a / b (they are the last op on their qubit)
         for q in (a, b):
             j = last.get(q)
