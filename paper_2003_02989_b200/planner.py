@@ -403,8 +403,8 @@ def build_ops(infos: list[GateInfo], adjoint: bool, block: bool = False) -> list
             continue
         new = Op(OP_DENSE2, (a, b), factors=[], symbolic=info.symbolic,
                  sym=info.sym if info.symbolic else -1)
-        if not adjoint and ABSORB_INTO_2Q:
-            # forward: every earlier op that lives on {a, b} alone and is not followed by an
+        if (not adjoint or block) and ABSORB_INTO_2Q:
+            # forward / block-fused adjoint: every earlier op that lives on {a, b} alone and is not followed by an
             # op linking a or b to another qubit joins the new 4x4 (1q runs, symbolic phase
             # gates on a / b / the pair): later ops touching them are absorbed too, ops on
             # other qubits commute with them
