@@ -66,9 +66,6 @@ TB_MODE = os.environ.get("QF_TB_MODE", "cs")
 # frame-normalised rotations of the adjoint take their gradient after the apply (rescaled);
 # measured slower on the headline (2.18 vs 2.09 ms per middle backward pass), off
 GRAD_AFTER = os.environ.get("QF_GRAD_AFTER", "0") not in ("0", "", "false")
-# adjoint dense 4x4: psi and lambda in one sweep, matrix rows re-read from shared memory
-# (measured on the QCNN backward: 28.5 vs 27.3 ms, off)
-PAIR_APPLY = os.environ.get("QF_PAIR_APPLY", "0") not in ("0", "", "false")
 STREAM_POLY = os.environ.get("QF_STREAM_POLY", "auto")   # auto: R >= 5 (measured: R = 4 keeps the WHT)
 
 
@@ -686,11 +683,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 elif kind == pl.OP_DENSE2:
                     if adj:
                         w("    {")
-                        if PAIR_APPLY:
-                            w(f"      apply2m_pair<{s0}, {s1}, {NR}>(v0, v1, MM + {moff});")
-                        else:
-                            w(f"      apply2m<{s0}, {s1}, {NR}>(v0, MM + {moff});"
-                              f" apply2m<{s0}, {s1}, {NR}>(v1, MM + {moff});")
+                        w(f"      apply2m<{s0}, {s1}, {NR}>(v0, MM + {moff});"
+                          f" apply2m<{s0}, {s1}, {NR}>(v1, MM + {moff});")
                         if slot >= 0 and int(op[13]):
                             o.extend(_block_code(4, 1 << s0, 1 << s1, slot - slb, gs_store, "      ", NR))
                         elif slot >= 0:
