@@ -136,6 +136,7 @@ typedef struct QfBuildRecipe {
   const double* term_const;      /* [const_rows, n_const] constant angles */
   int32_t const_rows;            /* 1 or rows */
   int32_t n_const;
+  int32_t max_dim;               /* largest dense_dim (threads per op in the build); 0 = 4 */
 } QfBuildRecipe;
 
 const char* qf_last_error(void);

@@ -43,7 +43,7 @@ class QfBuildRecipe(C.Structure):
         ("n_fixed", _i32), ("fixed", _p), ("fixed_rows", _i32),
         ("n_dense", _i32), ("dense_mat", _p), ("dense_dim", _p), ("dense_fbeg", _p), ("factor", _p),
         ("n_terms", _i32), ("term_src", _p), ("term_beta", _p), ("term_const", _p),
-        ("const_rows", _i32), ("n_const", _i32),
+        ("const_rows", _i32), ("n_const", _i32), ("max_dim", _i32),
     ]
 
 

@@ -87,9 +87,10 @@ __device__ __forceinline__ void factor_apply(const QfBuildRecipe& R, int kind, i
 __global__ void build_dense_col_kernel(const QfBuildRecipe R, const float* theta, int64_t tstride, int rows,
                                        float2* mats, int n_mat) {
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= (int64_t)rows * R.n_dense * 4) return;
-  const int col = (int)(id & 3);
-  const int64_t ro = id >> 2;
+  const int cols = R.max_dim == 2 ? 2 : 4;     // one-qubit-only programs: no idle column threads
+  if (id >= (int64_t)rows * R.n_dense * cols) return;
+  const int col = (int)(id & (cols - 1));
+  const int64_t ro = cols == 2 ? id >> 1 : id >> 2;
   const int row = (int)(ro / R.n_dense), op = (int)(ro % R.n_dense);
   const int D = R.dense_dim[op];
   if (col >= D) return;
@@ -631,7 +632,7 @@ int qf_build_ops(const QfBuildRecipe* recipe, const float* theta, int64_t theta_
   cudaStream_t s = (cudaStream_t)stream;
   const int T = 128;
   if (recipe->n_dense > 0 && rows > 0) {
-    const int64_t tot = (int64_t)rows * recipe->n_dense * 4;
+    const int64_t tot = (int64_t)rows * recipe->n_dense * (recipe->max_dim == 2 ? 2 : 4);
     build_dense_col_kernel<<<(unsigned)((tot + T - 1) / T), T, 0, s>>>(*recipe, theta, theta_stride, rows,
                                                                        reinterpret_cast<float2*>(mats), n_mat);
     if (check_launch("build_dense_col_kernel")) return 1;

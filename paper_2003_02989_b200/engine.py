@@ -93,6 +93,7 @@ class DeviceProgram:
         self.n_fixed = r["n_fixed"]
         self.n_const = r["n_const"]
         self.n_dense = len(r["dense_mat"])
+        self.max_dim = int(max(r["dense_dim"])) if len(r["dense_dim"]) else 0
         self.n_terms = len(r["term_beta"])
         self.tiles = 1 << (prog.n - prog.L)
         self._jit = None
@@ -143,6 +144,7 @@ class DeviceProgram:
             dense_dim=_ptr(a["dense_dim"]), dense_fbeg=_ptr(a["dense_fbeg"]), factor=_ptr(a["factor"]),
             n_terms=self.n_terms, term_src=_ptr(a["term_src"]), term_beta=_ptr(a["term_beta"]),
             term_const=_ptr(const_t), const_rows=const_rows, n_const=max(self.n_const, 1),
+            max_dim=self.max_dim,
         )
 
     def jit(self, device, rows: int, force: bool = False):
@@ -174,6 +176,7 @@ _JIT_LOCK = threading.Lock()
 # Measured: headline e2e 20.67k -> 20.78k circuits/s; cfg1 (1024 x 2^10) 0.49 -> 0.53 ms (the
 # replay's input copy and output clones outweigh 18 launches there) -> batches of at least
 # GRAPH_MIN_AMPS amplitudes only
+FRAME_MIN_AMPS = int(os.environ.get("QF_FRAME_MIN", str(1 << 24)))
 GRAPHS = os.environ.get("QF_GRAPH", "1") not in ("0", "", "false")
 MAX_GRAPHS = int(os.environ.get("QF_MAX_GRAPHS", "2"))
 GRAPH_MIN_AMPS = 1 << 22
@@ -278,9 +281,8 @@ class Bound:
                     M[k, j] += c
             self.hmix = torch.from_numpy(M).to(device)
             # weights of the default upstream (all ones): H_b = sum_k obs_k for every row
-            self.hw_ones = torch.from_numpy(np.ascontiguousarray(
-                np.broadcast_to(M.sum(axis=0, keepdims=True), (len(self.circuits), M.shape[1])))).to(
-                device=device, dtype=torch.float32)
+            self.hw_ones = torch.from_numpy(M.sum(axis=0, keepdims=True)).to(
+                device=device, dtype=torch.float32).expand(len(self.circuits), M.shape[1]).contiguous()
             self.lam_diag = bool(self.hkeys) and all(all(p == "Z" for _, p in kk) for kk in self.hkeys)
         # Pauli-frame normalisation (planner.build_program): only where every output is a
         # diagonal observable / adjoint gradient and the plan-specialised kernels run
@@ -289,6 +291,12 @@ class Bound:
         frame = (os.environ.get("QF_FRAME", "1") not in ("0", "", "false") and not want_state
                  and bool(obs.diag_ids) and not obs.generic_ids and (not want_grad or self.lam_diag)
                  and _jit.enabled(len(self.circuits), max(n, pl.N_MIN)))
+        if frame and "QF_FRAME" not in os.environ and "QF_JIT" not in os.environ and \
+                len(self.circuits) << max(n, pl.N_MIN) < FRAME_MIN_AMPS:
+            # the frame walk (one thread per row, sequential over the gates) costs a fixed
+            # ~0.1 ms; below 2^24 amplitudes it outweighs the FFMA2s it saves (cfg1 adjoint,
+            # 1024 x 2^10: 0.45 -> 0.31 ms without)
+            frame = False
         over = pl.batch_overrides(template, self.circuits, sym_index, pl.analyse(template, sym_index)) \
             if len(self.circuits) > 1 and not uniform else {}
         # block-fused adjoint (planner.build_ops(block=True)): plan-specialised kernels only
@@ -701,6 +709,10 @@ class Engine:
         infos = pl.analyse(template, symbol_index, overrides)
         if frame and adjoint:  # forward and adjoint must agree on the stored representation
             frame = pl.frame_eligible(pl.build_ops(pl.analyse(template, symbol_index, overrides), True), infos, True)
+        elif frame:
+            # forward only: no normalisable rotation (HEA runs fused into general 1q matrices,
+            # brickwork) -> no frame walk (it cost as much as the passes in cfg1's shifted batches)
+            frame = pl.has_normalisable(pl.build_ops(pl.analyse(template, symbol_index, overrides), False), infos)
         diag_sums = [None] * len(obs.sums)
         for k in obs.diag_ids:
             diag_sums[k] = _TermList(obs.sums[k])

@@ -246,10 +246,7 @@ def expectation_and_ps_gradient(circuits, symbol_names, symbol_values, operators
             return e_all, g_all
     vals_np = vals.detach().cpu().numpy().astype(np.float32).astype(np.float64).reshape(B, -1)
     col = {s: i for i, s in enumerate(symbol_names)}
-    e0 = expectation(circuits, symbol_names, vals, ops)
-    e0 = e0.detach().cpu().numpy() if isinstance(e0, torch.Tensor) else e0
     up = np.ones((B, len(ops))) if upstream is None else np.asarray(upstream, dtype=np.float64).reshape(B, -1)
-    grad = np.zeros((B, S))
     # rows sharing one circuit object share one expanded circuit (values differ only)
     groups: dict = {}
     for b, c in enumerate(circuits):
@@ -270,13 +267,21 @@ def expectation_and_ps_gradient(circuits, symbol_names, symbol_values, operators
         base = (coeff[None, :] * vals_np[bs][:, cols] + const[None, :]) * beta[None, :] if spec else None
         structs[key] = (ec, base, [(col[syms_c[si]], w) for si, w in occ])
     K = len(names0 or [])
+    dev = _device()
+    grad_d = None
     if K:
-        # shifted parameter rows [B, 2K, K] built on the device: row (b, 2k / 2k+1) is base[b]
-        # with pseudo-symbol k shifted by +/- pi/4
-        dev = _device()
+        # every host table goes to the device before the first launch (a pageable host->device
+        # copy waits for the stream, so a copy between launches idles the GPU)
         base_all = np.empty((B, K))
+        # gradient = d @ W per group: W[k, s] = sum of the occurrence weights of pseudo-symbol k
+        Ws = {}
         for key, bs in groups.items():
             base_all[bs] = structs[key][1]
+            W = np.zeros((K, S))
+            for k, (si, w) in enumerate(structs[key][2]):
+                W[k, si] += w
+            Ws[key] = torch.as_tensor(W, device=dev)
+        upd = torch.as_tensor(up, dtype=torch.float64, device=dev)
         rows = torch.as_tensor(base_all, dtype=torch.float64, device=dev)[:, None, :].repeat(1, 2 * K, 1)
         kk = torch.arange(K, device=dev)
         rows[:, 2 * kk, kk] += gr.SHIFT
@@ -292,19 +297,22 @@ def expectation_and_ps_gradient(circuits, symbol_names, symbol_values, operators
             else:
                 cs = [structs[id(circuits[r // (2 * K)])][0] for r in range(s0, s1)]
             f[s0:s1] = expectation(cs, names0, allrows[s0:s1], ops)
-        upd = torch.as_tensor(up, dtype=torch.float64, device=dev)
         f = (f.reshape(B, K, 2, len(ops)) * upd[:, None, None, :]).sum(dim=3)
-        d = (f[:, :, 0] - f[:, :, 1]).cpu().numpy()                     # [B, K]
-        for key, bs in groups.items():
-            occ = structs[key][2]
-            si = np.array([o[0] for o in occ], dtype=np.int64)
-            w = np.array([o[1] for o in occ], dtype=np.float64)
-            ix = np.asarray(bs, dtype=np.int64)
-            np.add.at(grad, (ix[:, None], si[None, :]), w[None, :] * d[ix])
+        d = f[:, :, 0] - f[:, :, 1]                                       # [B, K]
+        if len(groups) == 1:
+            grad_d = d @ Ws[next(iter(groups))]
+        else:
+            grad_d = torch.zeros((B, S), dtype=torch.float64, device=dev)
+            for key, bs in groups.items():
+                ix = torch.as_tensor(bs, device=dev)
+                grad_d[ix] = d[ix] @ Ws[key]
+    e0 = expectation(circuits, symbol_names, vals, ops)
+    if grad_d is None:
+        grad_d = torch.zeros((B, S), dtype=torch.float64, device=dev)
     if on_dev:
         dev = vals.device
-        return torch.as_tensor(e0, device=dev), torch.as_tensor(grad, device=dev)
-    return e0, grad
+        return torch.as_tensor(e0, device=dev), grad_d.to(dev)
+    return (e0.detach().cpu().numpy() if isinstance(e0, torch.Tensor) else e0), grad_d.cpu().numpy()
 
 
 def state(circuits, symbol_names, symbol_values):

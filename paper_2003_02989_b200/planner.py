@@ -975,6 +975,20 @@ def _walsh_angles(diag_entries: np.ndarray) -> np.ndarray:
     return a / d
 
 
+def has_normalisable(ops: list[Op], infos) -> bool:
+    """Does any op become a Pauli-frame normalised rotation?  Without one the frame stays the
+    identity (dense ops absorb it, diagonal ops see no x part) and the walk is wasted work."""
+    for o in ops:
+        if o.kind == OP_DENSE1:
+            axes = {infos[gi].axis for gi in o.factors}
+            if len(axes) == 1 and axes <= {"X", "Y"}:
+                return True
+        elif (o.kind == OP_DENSE2 and len(o.factors) == 1 and infos[o.factors[0]].symbolic
+              and bool(infos[o.factors[0]].pstring)):
+            return True
+    return False
+
+
 def frame_eligible(ops: list[Op], infos, adjoint: bool) -> bool:
     """Every program qualifies: normalised X/Y rotations carry their generator's frame sign
     in the slot scale; any other gradient-carrying dense op absorbs the frame into its matrix
@@ -1026,6 +1040,10 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         if n2 * 2 > len(ops):
             L, R = 11, 4   # FP32-bound dense programs: smaller tiles, more CTAs (RCS 24q: 162 vs 167 ms)
     L = min(L, n)
+    if L - R < 6 and "QF_GEOM_ADJ" not in __import__("os").environ and "QF_GEOM_FWD" not in __import__("os").environ:
+        # registers that cover the whole state: at least two warps per tile (cfg1 parameter-shift
+        # batches, 10 qubits: R = 4 12.7 ms vs R = 5 15.5 ms, R = 3 13.6 ms)
+        R = max(4, L - 6)
     frame = frame and frame_eligible(ops, infos, adjoint)
     if from_state and not adjoint:
         init = {}
@@ -1039,13 +1057,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     if frame and REMAP and jit and not adjoint and not mirror and not from_state and n > L:
         # a Pauli frame only pays off through normalised rotations; a program whose dense ops
         # would all absorb it (brickwork / RCS) is relabelled instead
-        def _normalisable(o):
-            if o.kind == OP_DENSE1:
-                axes = {infos[gi].axis for gi in o.factors}
-                return len(axes) == 1 and axes <= {"X", "Y"}
-            return (o.kind == OP_DENSE2 and len(o.factors) == 1 and infos[o.factors[0]].symbolic
-                    and bool(infos[o.factors[0]].pstring))
-        if not any(_normalisable(o) for o in ops):
+        if not has_normalisable(ops, infos):
             frame = False
     remap = (REMAP and jit and not adjoint and not mirror and not from_state and not frame and n > L)
     tc_ok = TC_STAGES and jit and not adjoint and not mirror and R == 4 and L - R == 7

@@ -37,6 +37,9 @@ def programs(name):
     elif name == "hea":
         circ = wl.hea_circuit(16, 4)
         cost = wl.z_sum(16)
+    elif name == "hea10":   # cfg1's size (the parameter-shift batches run forward programs only)
+        circ = wl.hea_circuit(10, 4)
+        cost = wl.z_sum(10)
     else:
         raise SystemExit(f"unknown workload {name}")
     syms = circuit_symbols(circ) if name != "qcnn" else circuit_symbols(model)
@@ -45,8 +48,9 @@ def programs(name):
     infos = pl.analyse(circ, si)
     n = circ.num_qubits
     frame = os.environ.get("QF_FRAME", "1") != "0"
+    frame_fwd = frame and pl.has_normalisable(pl.build_ops(pl.analyse(circ, si), False), pl.analyse(circ, si))
     fwd = pl.build_program(circ, infos, n, adjoint=False, observables=[_TermList(obs.sums[0])], obs_diag_ids=[0],
-                           frame=frame)
+                           frame=frame_fwd if os.environ.get("QF_SASS_FWD_ONLY") else frame)
     hk = [tuple(sorted(t.factors.items())) for t in obs.sums[0]]
     lam_diag = all(all(p == "Z" for _, p in k) for k in hk)
     adj = pl.build_program(circ, pl.analyse(circ, si), n, adjoint=True,
