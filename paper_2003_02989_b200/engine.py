@@ -727,7 +727,7 @@ class Engine:
                 os.environ.get("QF_CKPT", "1") not in ("0", "", "false"):
             fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
                                    obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame, mirror=True,
-                                   block=block)
+                                   block=block, vec=jit)
             # the adjoint's backward pass i must undo exactly forward pass P-1-i (both lists
             # are in forward order), and both frame walks must hold the same Pauli frame at every
             # pass boundary: true for normalised rotations and diagonal ops, not for general
@@ -743,7 +743,7 @@ class Engine:
             # which loads the forward's output in the identity layout
             fwd = pl.build_program(template, infos, n_eff, adjoint=False, observables=diag_sums,
                                    obs_diag_ids=obs.diag_ids, from_state=from_state, frame=frame,
-                                   jit=jit and not adjoint)
+                                   jit=jit and not adjoint, vec=jit)
         plan = Plan(n, n_eff, len(symbol_index), infos, DeviceProgram(fwd, device), None, lam_diag, obs)
         plan.extra["from_state"] = from_state
         plan.extra["ckpt"] = ckpt

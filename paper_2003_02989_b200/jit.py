@@ -61,6 +61,12 @@ EXP_MODE = os.environ.get("QF_EXP", "")
 # (measured: "cs" is faster, forward middle passes 0.93 -> 0.86 ms on the headline)
 # "cs" 8-byte (c, s) entries (half the shared-memory bytes, one FADD per lookup)
 TB_MODE = os.environ.get("QF_TB_MODE", "cs")
+# L2 prefetch of the tile the next wave of CTAs will load (cp.async.bulk.prefetch.L2, issued
+# right after this tile's own loads): 0 off, 1 adjoint passes, 2 every pass
+L2PF = int(os.environ.get("QF_L2PF", "0") or 0)
+# a barrier before each inner exchange's writes (not needed: see generate)
+PREW_SYNC = os.environ.get("QF_PREW_SYNC", "0") not in ("0", "", "false")
+L2PF_SMS = int(os.environ.get("QF_L2PF_SMS", "148"))
 # integer-weight phase polynomials evaluated per amplitude in Gray-code order (one live value)
 # instead of by a 2^R-entry Walsh transform
 # frame-normalised rotations of the adjoint take their gradient after the apply (rescaled);
@@ -501,11 +507,23 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 w(f"  const float2* __restrict__ pt0 = (a.psi_src ? a.psi_src + ((size_t)row << {n}) : psi) + gt0;")
             if adj and init == pl.INIT_LOAD:
                 w("  const float2* __restrict__ lt0 = lam + gt0;")
+            vec_ld = int(st0[0]) == 0 and EXP_MODE != "noload"
             for r in range(NR):
                 if EXP_MODE == "noload":
                     w(f"  v0[{r}] = make_float2((float)(gt0 + {r}u) * 1e-9f, 0.5f);")
                     if adj:
                         w(f"  v1[{r}] = make_float2(0.25f, (float)(gt0 ^ {r}u) * 1e-9f);")
+                    continue
+                if vec_ld:
+                    # register slot 0 is qubit 0: amplitudes (x, x | 1) in one 16-byte load
+                    if r & 1:
+                        continue
+                    w(f"  ld_pair(pt0 + {roff(st0, r)}ll, v0[{r}], v0[{r + 1}]);")
+                    if adj:
+                        if init == pl.INIT_LOAD:
+                            w(f"  ld_pair(lt0 + {roff(st0, r)}ll, v1[{r}], v1[{r + 1}]);")
+                        else:
+                            w(f"  v1[{r}] = make_float2(0.f, 0.f); v1[{r + 1}] = make_float2(0.f, 0.f);")
                     continue
                 w(f"  v0[{r}] = pt0[{roff(st0, r)}ll];")
                 if adj:
@@ -536,6 +554,29 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     w(f"    v0[{r | (1 << j)}] = cmul(v0[{r}], f1); v0[{r}] = cmul(v0[{r}], f0);")
                 w("  }")
 
+        if (L2PF >= (1 if adj else 2) and not PERSIST and fuse != "tail" and EXP_MODE != "noload"
+                and init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI)):
+            c_run = 0
+            while c_run < L and tileq[c_run] == c_run:
+                c_run += 1
+            if c_run >= 4:
+                runs = 1 << (L - c_run)
+                ahead = int(os.environ.get("QF_L2PF_AHEAD", "0")) or minb_p * L2PF_SMS
+                nb_ = " | ".join(f"(((no >> {i}) & 1u) << {q})" for i, q in enumerate(outer)) or "0u"
+                offx = _xor_expr([1 << tileq[c_run + j] for j in range(L - c_run)], "i") if runs > 1 else "0u"
+                srcs_ = ["a.psi"] if adj else ["(a.psi_src ? a.psi_src : a.psi)"]
+                if adj and init == pl.INIT_LOAD:
+                    srcs_.append("a.lam")
+                w(f"  {{ const u32 nb = blockIdx.x + {ahead}u;")
+                w("    if (nb < gridDim.x) {")
+                w(f"      const u32 nrow = nb >> {n - L}, no = nb & {(1 << (n - L)) - 1}u;")
+                w(f"      const u32 nbase = {nb_};")
+                w(f"      for (u32 i = t; i < {runs}u; i += {NT}u) {{ const u32 off = nbase | ({offx});")
+                for s_ in srcs_:
+                    w(f"        l2_prefetch_bulk({s_} + ((size_t)nrow << {n}) + off, {8 << c_run}u);")
+                w("      }")
+                w("    }")
+                w("  }")
         mark_load_end = len(o)
         if not PERSIST and not prefetch and not adj and init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI):
             # (forward sweep only: measured slower for the adjoint)
@@ -549,9 +590,11 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         for si, st in enumerate(st_rows if EXP_MODE != "memonly" else []):
             if si:
                 prev = st_rows[si - 1]
-                if si > 1 or PERSIST:
-                    # readers of the previous exchange must be done before it is overwritten
-                    # (the first exchange of a tile has no earlier readers of this buffer)
+                if PERSIST or (si > 1 and (PREW_SYNC or tc_stages)):
+                    # readers of the previous exchange must be done before it is overwritten.
+                    # Without it: a thread writes exactly the addresses it read itself in the
+                    # previous exchange (both in layout `prev`), so there is no cross-thread
+                    # hazard; the first exchange of a tile has no earlier readers at all
                     w("  __syncthreads();")
                 w(f"  {{ const u32 tp = {_xor_expr(tphys(prev))};")
                 for r in range(NR):
@@ -946,15 +989,23 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 w("    float2* __restrict__ pts = psi + gs;")
             if adj and pi != remote_pass:
                 w("    float2* __restrict__ lts = lam + gs;")
+            # register slot 0 is qubit 0: amplitudes (x, x | 1) in one 16-byte store
+            vec_st = int(stl[0]) == 0 and not int(p[126])
+
+            def st_all(ptr, v, ind):
+                for r in range(NR):
+                    if vec_st:
+                        if not r & 1:
+                            w(f"{ind}st_pair({ptr} + {roff(stl, r)}ll, {v}[{r}], {v}[{r + 1}]);")
+                    else:
+                        w(f"{ind}{ptr}[{roff(stl, r)}ll] = {v}[{r}];")
             if adj and pi != remote_pass:
                 w("    if (!a.skip_psi) {")
-                for r in range(NR):
-                    w(f"      pts[{roff(stl, r)}ll] = v0[{r}];")
+                st_all("pts", "v0", "      ")
                 w("    }")
-                for r in range(NR):
-                    w(f"    lts[{roff(stl, r)}ll] = v1[{r}];")
-            for r in (range(NR) if (pi != remote_pass and not adj) else []):
-                w(f"    pts[{roff(stl, r)}ll] = v0[{r}];")
+                st_all("lts", "v1", "    ")
+            if pi != remote_pass and not adj:
+                st_all("pts", "v0", "    ")
             w("  }")
         if scnt and chunked:
             if scnt % 16:

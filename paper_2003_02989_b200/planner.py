@@ -689,23 +689,33 @@ def plan_passes_remap(ops: list[Op], n: int, L: int) -> list[Pass]:
     return passes
 
 
-def _stage_regs(need: set, R: int, L: int, allow_lanes: bool, prefer: list) -> list:
+def _stage_regs(need: set, R: int, L: int, lanes: set, prefer: list) -> list:
     regs = set(need)
     for b in prefer + list(range(L - 1, -1, -1)):
         if len(regs) >= R:
             break
-        if b in regs or (not allow_lanes and b < LANE_Q):
+        if b in regs or b in lanes:
             continue
         regs.add(b)
     return sorted(regs)
 
 
-def plan_stages(p: Pass, R: int) -> None:
+def plan_stages(p: Pass, R: int, vec: bool = False) -> None:
+    """Register stages of one tile pass.  ``vec``: 16-byte edge accesses -- the first and
+    (where its registers allow) the last stage hold local bit 0 = qubit 0 in register slot 0
+    and take local bits 1..LANE_Q as lanes, so a thread loads / stores amplitude pairs
+    (x, x | 1) as one float4 (LDG.128 / STG.128, 256-byte runs per 16 lanes)."""
     L = len(p.qubits)
     loc = {q: i for i, q in enumerate(p.qubits)}
     ops = p.ops
     sch = _Sched(ops)
     stages: list[Stage] = []
+    # only where local bits 0..LANE_Q are qubits 0..LANE_Q (runs of >= 256 bytes): on tiles with
+    # 128-byte runs the pair layout spreads a warp over twice as many runs and measured slower
+    # (headline forward passes 1/3: 0.748 -> 0.830 ms; contiguous pass 2: 0.802 -> 0.796 ms,
+    # backward pass 2: 2.118 -> 2.067 ms)
+    vec = vec and p.out_pos is None and list(p.qubits[:LANE_Q + 1]) == list(range(LANE_Q + 1)) and L - R > LANE_Q
+    edge_lanes = set(range(1, LANE_Q + 1)) if vec else set(range(LANE_Q))
 
     def local_set(o):
         return {loc[q] for q in o.qubits}
@@ -713,7 +723,7 @@ def plan_stages(p: Pass, R: int) -> None:
     while sch.left > 0:
         first = not stages
         # choose register bits: greedily cover ready dense ops (in index order)
-        need: set = set()
+        need: set = {0} if (first and vec) else set()
         virt = _Sched(ops, subset=[j for j in range(len(ops)) if j in sch.npred and sch.npred.get(j, 0) >= 0])
         # replay the real state into the virtual scheduler
         virt.npred = dict(sch.npred)
@@ -729,7 +739,7 @@ def plan_stages(p: Pass, R: int) -> None:
                     progressed = True
                     break
                 ls = local_set(o)
-                if first and min(ls) < LANE_Q:
+                if first and ls & edge_lanes:
                     continue
                 if len(need | ls) <= R:
                     need |= ls
@@ -743,14 +753,28 @@ def plan_stages(p: Pass, R: int) -> None:
             for b in sorted(local_set(ops[j])):
                 if b not in upcoming:
                     upcoming.append(b)
-        regs = _stage_regs(need, R, L, allow_lanes=not first, prefer=[b for b in upcoming if b >= LANE_Q])
+        regs = _stage_regs(need, R, L, lanes=edge_lanes if first else set(),
+                           prefer=[b for b in upcoming if b not in edge_lanes])
         rs = set(regs)
         taken = sch.drain(lambda o: o.kind in (OP_DIAG, OP_OBS) or local_set(o) <= rs)
         stages.append(Stage(regs, taken))
         if not taken and not first:
             raise AssertionError("stage planner made no progress")
     if not stages:
-        stages.append(Stage(list(range(L - R, L)), []))
+        stages.append(Stage(sorted({0} | set(range(L - R + 1, L))) if vec else list(range(L - R, L)), []))
+    if vec:
+        # 16-byte stores from the last stage when its ops leave local bit 0 a register slot
+        # and keep off the lanes 1..LANE_Q (else the 8-byte store rule below)
+        last = stages[-1]
+        used = set()
+        for o in last.ops:
+            if o.kind not in (OP_DIAG, OP_OBS):
+                used |= local_set(o)
+        if not used & edge_lanes and (0 in used or len(used) < R):
+            last.regs = _stage_regs(used | {0}, R, L, lanes=edge_lanes,
+                                    prefer=[b for b in last.regs if b not in edge_lanes])
+            p.stages = stages
+            return
     # the store needs lanes on the local bits stored to physical 0..3: local 0..3, or for a
     # relabelled pass the bits whose out_pos < 4 (then the load and store stages differ)
     sl = store_lanes(p)
@@ -798,6 +822,8 @@ CONFLICT_FREE_LANES = __import__("os").environ.get("QF_LANE_ORDER", "1") not in 
 # cfg4 22 -> 14 passes but 162 -> 186 ms -- dense brickwork passes are FMA-bound (217 fused
 # blocks x 8 FFMA2 per amplitude = 0.40 s floor at 32 qubits), so fewer HBM passes buy little
 # and the extra store stages cost more; off by default
+# 16-byte edge loads / stores in plan-specialised kernels (plan_stages ``vec``)
+VEC_EDGE = __import__("os").environ.get("QF_VEC_EDGE", "1") not in ("0", "", "false")
 REMAP = __import__("os").environ.get("QF_REMAP", "0") not in ("0", "", "false")
 # tensor-core stages (csrc/qf_tc.cu): forward dense programs at 16 x 128 amplitudes per tile;
 # a stage qualifies when its dense work is at least TC_MIN_FFMA2 FFMA2 per amplitude.
@@ -1005,7 +1031,7 @@ def block_slots(D: int) -> int:
 def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool,
                   observables=None, obs_diag_ids=(), lam_diag: bool = False,
                   from_state: bool = False, frame: bool = False, mirror: bool = False,
-                  block: bool = False, jit: bool = False) -> Program:
+                  block: bool = False, jit: bool = False, vec: bool = None) -> Program:
     """Plan + emit.  ``observables``: list of PauliSums; ``obs_diag_ids``: those fused as
     OBS ops at the end of the forward program; ``lam_diag``: adjoint with a diagonal H
     whose lambda-init / energy is fused into the first backward pass; ``from_state``:
@@ -1016,7 +1042,11 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     amplitude); the stored state is psi = sqrt(m) X^x Z^z psi_stored up to a global phase,
     and the per-row frame (x, z, m) is tracked by the build step in execution order:
     general dense ops absorb the frame into their matrix, diagonal ops / observables are
-    evaluated at index ^ x, and slot sums are scaled by m (and the generator's sign)."""
+    evaluated at index ^ x, and slot sums are scaled by m (and the generator's sign).
+
+    ``vec``: the program runs as plan-specialised kernels (16-byte edge accesses,
+    plan_stages); default ``jit``."""
+    vec = jit if vec is None else vec
     # mirror: a forward program with exactly the adjoint program's ops and tile passes (no
     # symbolic fusion, adjoint tile size), so its pass outputs are checkpoints the adjoint
     # sweep can read and both Pauli-frame walks agree at every pass boundary
@@ -1072,7 +1102,7 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         for q, o in zip(passes[-1].qubits, passes[-1].out_pos):
             final_pos[q] = o
     for p in passes:
-        plan_stages(p, R)
+        plan_stages(p, R, vec=VEC_EDGE and vec)
     if obs_ops:
         passes[-1].stages[-1].ops.extend(obs_ops)
     if adjoint and lam_diag:

@@ -50,7 +50,7 @@ def programs(name):
     frame = os.environ.get("QF_FRAME", "1") != "0"
     frame_fwd = frame and pl.has_normalisable(pl.build_ops(pl.analyse(circ, si), False), pl.analyse(circ, si))
     fwd = pl.build_program(circ, infos, n, adjoint=False, observables=[_TermList(obs.sums[0])], obs_diag_ids=[0],
-                           frame=frame_fwd if os.environ.get("QF_SASS_FWD_ONLY") else frame)
+                           frame=frame_fwd if os.environ.get("QF_SASS_FWD_ONLY") else frame, vec=True)
     hk = [tuple(sorted(t.factors.items())) for t in obs.sums[0]]
     lam_diag = all(all(p == "Z" for _, p in k) for k in hk)
     adj = pl.build_program(circ, pl.analyse(circ, si), n, adjoint=True,
