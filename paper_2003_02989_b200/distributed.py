@@ -348,11 +348,18 @@ class NcclExchange:
             raise ValueError(f"{world} ranks cannot hold 2^{g} shards")
         self.g = g
         self.ranks = [dist.get_rank(group)]
+        # gloo (CPU tests, or several ranks sharing one GPU in the GPU tests) moves host
+        # tensors: device shards are staged through host memory, and no symmetric memory
+        self.host_staged = dist.get_backend(group) == "gloo"
         self._spare = None
         self._symm = None          # [(buffer, handle, peer-pointer tensor)] x 2, or False
         self._hdl = None
 
     def _symm_buffers(self, shape, dtype, device):
+        import os
+
+        if self.host_staged or os.environ.get("QF_SYMM", "1") in ("0", "", "false"):
+            self._symm = False
         if self._symm is False:
             return None
         if self._symm is not None and self._symm[0][0].shape == shape:
@@ -390,11 +397,21 @@ class NcclExchange:
         if self._spare is None or self._spare.shape != psi.shape:
             self._spare = psi.new_empty(psi.shape)
         out = self._spare
-        self.dist.all_to_all_single(_flat(out), _flat(psi), group=self.group)
+        if self.host_staged and psi.is_cuda:
+            h_out = out.cpu()
+            self.dist.all_to_all_single(_flat(h_out), _flat(psi.cpu()), group=self.group)
+            out.copy_(h_out)
+        else:
+            self.dist.all_to_all_single(_flat(out), _flat(psi), group=self.group)
         self._spare = psi
         return out
 
     def allreduce_sum(self, x):
+        if self.host_staged and x.is_cuda:
+            h = x.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            x.copy_(h)
+            return x
         self.dist.all_reduce(x, group=self.group)
         return x
 

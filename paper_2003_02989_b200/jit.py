@@ -66,6 +66,8 @@ TB_MODE = os.environ.get("QF_TB_MODE", "cs")
 L2PF = int(os.environ.get("QF_L2PF", "0") or 0)
 # a barrier before each inner exchange's writes (not needed: see generate)
 PREW_SYNC = os.environ.get("QF_PREW_SYNC", "0") not in ("0", "", "false")
+SPLIT_XCHG = os.environ.get("QF_SPLIT_XCHG", "0") not in ("0", "", "false")
+SPLIT_LIGHT_OPS = int(os.environ.get("QF_SPLIT_LIGHT_OPS", "12"))
 L2PF_SMS = int(os.environ.get("QF_L2PF_SMS", "148"))
 # integer-weight phase polynomials evaluated per amplitude in Gray-code order (one live value)
 # instead of by a 2^R-entry Walsh transform
@@ -205,6 +207,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
     TB = L - R
     NR, NT = 1 << R, 1 << TB
     NA = 2 if adj else 1
+    # adjoint exchanges psi and lambda one after the other through one tile buffer (half the
+    # shared memory per CTA, two more barriers per exchange)
     TILE = 1 << L
     env_minb = int(os.environ.get("QF_MINB_ADJ" if adj else "QF_MINB_FWD", "0"))
     # measured best (tools/sweep.sh): 128 registers for the 12/5 forward (4 CTAs x 128
@@ -248,7 +252,15 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         GSW = NT if (per_thread_gs or chunked) else NT // 32
         ws_floats = (NT // 32) * 32 if (scnt and (per_thread_gs or chunked)) else 0
         gs_slots = min(scnt, 16) if chunked else scnt
-        smem = NA * TILE * 8 + mcnt * 16 + acnt * 4 + ccnt * 4 + gs_slots * GSW * 4 + ws_floats * 4 + 16
+        n_gate_ops = sum(int(prog.ops[k_][0]) in (pl.OP_DENSE1, pl.OP_DENSE2) for k_ in pass_op_ids)
+        # light backward passes of the R = 5 rotation programs (the turn kernel's backward part,
+        # the last backward pass): psi and lambda exchanged one after the other through one tile
+        # buffer, 3 CTAs/SM (measured on the headline: turn 1.40 -> 1.29 ms, last pass 1.33 ->
+        # 1.31 ms; the 20-op middle passes spill at 168 registers and lose, 2.07 -> 2.26 ms)
+        light = (adj and R == 5 and L == 12 and not env_minb and SPLIT_LIGHT_OPS > 0 and not PERSIST
+                 and n_gate_ops <= SPLIT_LIGHT_OPS)
+        NX = 1 if (adj and (SPLIT_XCHG or light)) else NA
+        smem = NX * TILE * 8 + mcnt * 16 + acnt * 4 + ccnt * 4 + gs_slots * GSW * 4 + ws_floats * 4 + 16
         # integer-weight phase polynomials (full-WHT path only) get a per-CTA phase table
         int_tables = {}
         tbl_bytes = 0
@@ -291,6 +303,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         heavy = any(int(op_[0]) == pl.OP_DENSE2 or (int(op_[0]) == pl.OP_DENSE1 and int(op_[9]) == pl.CLS_GENERAL)
                     for op_ in pass_ops)
         minb_p = min(minb, max(1, 65536 // (NT * 128))) if (heavy and not env_minb) else minb
+        if light:
+            minb_p = 3
         n_dense2 = sum(int(op_[0]) == pl.OP_DENSE2 for op_ in pass_ops)
         if not adj and R == 5 and n_dense2 >= 4 and not env_minb:
             # 32 amplitudes per thread plus 4x4 matrices spill at 128 registers: 168 (3 CTAs/SM)
@@ -333,7 +347,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         w("  float2* sm = reinterpret_cast<float2*>(smem_raw);")
         # staged matrices: one 16-byte entry {Re, Im, -Im, Im} per element, so a dense apply
         # reads the broadcast real part and the (-Im, Im) pair with one LDS.128
-        w(f"  float4* MM = reinterpret_cast<float4*>(sm + {NA * TILE});")
+        w(f"  float4* MM = reinterpret_cast<float4*>(sm + {NX * TILE});")
         w(f"  int* ANG = reinterpret_cast<int*>(MM + {mcnt});")
         w(f"  float* CO = reinterpret_cast<float*>(ANG + {acnt});")
         w(f"  float* GS = CO + {ccnt};")
@@ -596,19 +610,33 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     # previous exchange (both in layout `prev`), so there is no cross-thread
                     # hazard; the first exchange of a tile has no earlier readers at all
                     w("  __syncthreads();")
-                w(f"  {{ const u32 tp = {_xor_expr(tphys(prev))};")
-                for r in range(NR):
-                    w(f"    sm[tp ^ {roff(prev, r, True)}u] = v0[{r}];")
-                    if adj:
-                        w(f"    sm[{TILE} + (tp ^ {roff(prev, r, True)}u)] = v1[{r}];")
-                w("  }")
-                w("  __syncthreads();")
-                w(f"  {{ const u32 tp = {_xor_expr(tphys(st))};")
-                for r in range(NR):
-                    w(f"    v0[{r}] = sm[tp ^ {roff(st, r, True)}u];")
-                    if adj:
-                        w(f"    v1[{r}] = sm[{TILE} + (tp ^ {roff(st, r, True)}u)];")
-                w("  }")
+                if NX == 1 and adj:
+                    for vv in ("v0", "v1"):
+                        if vv == "v1":
+                            w("  __syncthreads();")
+                        w(f"  {{ const u32 tp = {_xor_expr(tphys(prev))};")
+                        for r in range(NR):
+                            w(f"    sm[tp ^ {roff(prev, r, True)}u] = {vv}[{r}];")
+                        w("  }")
+                        w("  __syncthreads();")
+                        w(f"  {{ const u32 tp = {_xor_expr(tphys(st))};")
+                        for r in range(NR):
+                            w(f"    {vv}[{r}] = sm[tp ^ {roff(st, r, True)}u];")
+                        w("  }")
+                else:
+                    w(f"  {{ const u32 tp = {_xor_expr(tphys(prev))};")
+                    for r in range(NR):
+                        w(f"    sm[tp ^ {roff(prev, r, True)}u] = v0[{r}];")
+                        if adj:
+                            w(f"    sm[{TILE} + (tp ^ {roff(prev, r, True)}u)] = v1[{r}];")
+                    w("  }")
+                    w("  __syncthreads();")
+                    w(f"  {{ const u32 tp = {_xor_expr(tphys(st))};")
+                    for r in range(NR):
+                        w(f"    v0[{r}] = sm[tp ^ {roff(st, r, True)}u];")
+                        if adj:
+                            w(f"    v1[{r}] = sm[{TILE} + (tp ^ {roff(st, r, True)}u)];")
+                    w("  }")
             reg_glob = [int(st[j]) for j in range(R)]
             need_gt = any(int(prog.ops[k][0]) in (pl.OP_DIAG, pl.OP_OBS) for k in range(int(st[48]), int(st[49])))
             if need_gt:
