@@ -68,6 +68,7 @@ L2PF = int(os.environ.get("QF_L2PF", "0") or 0)
 PREW_SYNC = os.environ.get("QF_PREW_SYNC", "0") not in ("0", "", "false")
 SPLIT_XCHG = os.environ.get("QF_SPLIT_XCHG", "0") not in ("0", "", "false")
 SPLIT_LIGHT_OPS = int(os.environ.get("QF_SPLIT_LIGHT_OPS", "12"))
+ADJ3 = os.environ.get("QF_ADJ3", "0") not in ("0", "", "false")
 L2PF_SMS = int(os.environ.get("QF_L2PF_SMS", "148"))
 # integer-weight phase polynomials evaluated per amplitude in Gray-code order (one live value)
 # instead of by a 2^R-entry Walsh transform
@@ -245,14 +246,18 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 merged_last[int(prog.ops[k_][7])] = k_
         # slot partials: one float per thread and slot, or (many slots) one per warp after a
         # shuffle reduction, so the CTA keeps its occupancy
-        per_thread_gs = scnt * NT * 4 <= GS_THREAD_BYTES
+        n_gate_ops = sum(int(prog.ops[k_][0]) in (pl.OP_DENSE1, pl.OP_DENSE2) for k_ in pass_op_ids)
+        # heavy backward passes of the R = 5 rotation programs at 3 CTAs/SM (QF_ADJ3): 168
+        # registers, slot partials in a 12-slot ring so that three CTAs' shared memory fits
+        adj3 = adj and R == 5 and L == 12 and ADJ3 and not env_minb and not PERSIST and n_gate_ops > SPLIT_LIGHT_OPS
+        per_thread_gs = scnt * NT * 4 <= GS_THREAD_BYTES and not (adj3 and scnt > 12)
+        RING = 12 if adj3 else 16
         # many slots: a ring of 16 per-thread slots flushed by a 16-value warp transpose-reduction
         # (slots must then be stored in slot order: not with merged accumulators)
         chunked = (not per_thread_gs) and CHUNKED_GS and NT >= 64 and not merged_last
         GSW = NT if (per_thread_gs or chunked) else NT // 32
         ws_floats = (NT // 32) * 32 if (scnt and (per_thread_gs or chunked)) else 0
-        gs_slots = min(scnt, 16) if chunked else scnt
-        n_gate_ops = sum(int(prog.ops[k_][0]) in (pl.OP_DENSE1, pl.OP_DENSE2) for k_ in pass_op_ids)
+        gs_slots = min(scnt, RING) if chunked else scnt
         # light backward passes of the R = 5 rotation programs (the turn kernel's backward part,
         # the last backward pass): psi and lambda exchanged one after the other through one tile
         # buffer, 3 CTAs/SM (measured on the headline: turn 1.40 -> 1.29 ms, last pass 1.33 ->
@@ -303,7 +308,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         heavy = any(int(op_[0]) == pl.OP_DENSE2 or (int(op_[0]) == pl.OP_DENSE1 and int(op_[9]) == pl.CLS_GENERAL)
                     for op_ in pass_ops)
         minb_p = min(minb, max(1, 65536 // (NT * 128))) if (heavy and not env_minb) else minb
-        if light:
+        if light or adj3:
             minb_p = 3
         n_dense2 = sum(int(op_[0]) == pl.OP_DENSE2 for op_ in pass_ops)
         if not adj and R == 5 and n_dense2 >= 4 and not env_minb:
@@ -334,9 +339,9 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             if per_thread_gs:
                 return f"GS[{slot_rel * NT} + t] = {expr};"
             if chunked:
-                st = f"GS[{(slot_rel % 16) * NT} + t] = {expr};"
-                if slot_rel % 16 == 15:
-                    st += " " + gs_flush(slot_rel - 15, 16)
+                st = f"GS[{(slot_rel % RING) * NT} + t] = {expr};"
+                if slot_rel % RING == RING - 1:
+                    st += " " + gs_flush(slot_rel - (RING - 1), RING)
                 return st
             return f"{{ const float gsv = warp_sum_f({expr}); if ((t & 31u) == 0u) GS[{slot_rel * GSW} + (t >> 5)] = gsv; }}"
         geo.append((NT, smem))
@@ -1036,8 +1041,8 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 st_all("pts", "v0", "    ")
             w("  }")
         if scnt and chunked:
-            if scnt % 16:
-                w("  " + gs_flush(scnt - scnt % 16, scnt % 16))
+            if scnt % RING:
+                w("  " + gs_flush(scnt - scnt % RING, scnt % RING))
         elif scnt and per_thread_gs and NT >= 64:
             # each thread's slot values are its own GS entries: per 32-slot chunk, a warp
             # transpose-reduction leaves slot L's warp sum on lane L; warps combine in order
