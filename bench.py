@@ -198,8 +198,7 @@ def _blas_threads():
 
 class CpuReference:
     """The reference's CPU path (oracle port) on every host core: a pool of single-threaded
-    processes, each step = one evaluation per core, walking through row 0's 401 evaluations
-    (1 expectation + 400 parameter-shift); at least one full row is always timed."""
+    processes walking through row 0's 401 evaluations (1 expectation + 400 parameter-shift)."""
 
     def __init__(self, cores):
         import multiprocessing as mp
@@ -210,10 +209,10 @@ class CpuReference:
         self.n_evals = len(_row_jobs()[2])
         self.next = 0
 
-    def step(self):
-        ids = list(range(self.next, self.next + self.cores))
-        self.next += self.cores
-        return self.pool.map(_cpu_eval, ids, chunksize=1)
+    def step(self, per_core=1):
+        ids = list(range(self.next, self.next + self.cores * per_core))
+        self.next += len(ids)
+        return self.pool.map(_cpu_eval, ids, chunksize=per_core)
 
     def close(self):
         self.pool.close()
@@ -222,27 +221,29 @@ class CpuReference:
 
 def cpu_reference_rate(cores: int, steps: int = 1, warmup: int = 1):
     """circuits/s of the reference path (expectation + parameter-shift gradient per row) on
-    ``cores`` processes; times max(steps, ceil(401 / cores)) steps so that at least one full
-    row's evaluations are covered."""
+    ``cores`` processes.  Exactly ``steps`` timed steps; one step = ceil(401 / (steps * cores))
+    evaluations per core, so the timed steps always cover at least one full row's evaluations.
+    Warm-up steps (untimed) are one evaluation per core."""
     ref = CpuReference(cores)
+    steps = max(int(steps), 1)
+    per_core = -(-ref.n_evals // (steps * cores))
     try:
         for _ in range(max(warmup, 0)):
             ref.pool.map(_cpu_eval, [0] * cores, chunksize=1)    # imports + first-touch, untimed
-        n_steps = max(steps, -(-ref.n_evals // cores))
         t0 = time.perf_counter()
         per = []
-        for _ in range(n_steps):
-            per += ref.step()
+        for _ in range(steps):
+            per += ref.step(per_core)
         wall = time.perf_counter() - t0
     finally:
         ref.close()
-    evals = n_steps * cores
+    evals = steps * cores * per_core
     rate = evals / wall / ref.n_evals            # rows (circuits) per second, all cores
     return rate, dict(t_eval_s=float(np.mean(per)), evals_per_circuit=ref.n_evals, wall_s=wall,
-                      row_s=ref.n_evals * wall / evals, steps=n_steps, blas_threads=_blas_threads(),
+                      row_s=ref.n_evals * wall / evals, steps=steps, per_core=per_core, blas_threads=_blas_threads(),
                       sample=f"{evals} evaluations ({evals / ref.n_evals:.2f} full 20q rows: 1 expectation + "
                              f"{ref.n_evals - 1} parameter-shift evaluations each) on {cores} single-threaded "
-                             f"processes, {n_steps} steps of one evaluation per core")
+                             f"processes, {steps} steps of {per_core} evaluation(s) per core")
 
 
 def run_reference(args, rank, world):
@@ -257,7 +258,8 @@ def run_reference(args, rank, world):
         "impl": "reference",
         "config": {"workload": "qaoa_maxcut_20q_p4_b256", "global_batch": BATCH, "n_qubits": N_QUBITS,
                    "depth": DEPTH, "gradient": "parameter-shift (reference has no adjoint)",
-                   "step": "one 20q evaluation per host core"},
+                   "step": f"{info['per_core']} 20q evaluation(s) per host core ({cores} cores): the "
+                           f"{args.steps} timed steps cover >= one full row"},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": info["sample"],
                          "row_s": info["row_s"], "eval_s": info["t_eval_s"], "blas_threads": info["blas_threads"]},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
