@@ -168,3 +168,69 @@ def test_cfg5_brickwork28_vs_cpu_reference(cuda):
     st = ops.state(circ, [], th0)
     idx = torch.as_tensor(arr["amp_idx"], device="cuda")
     np.testing.assert_allclose(st[0, idx].cpu().numpy(), arr["amps"], atol=AMP)
+
+
+# ---------------------------------------------------------------------------
+# every row of the full-size batches: size-independent properties between independent
+# code paths (the adjoint sweep vs the reference's parameter-shift rule, both on the GPU;
+# state norms; sampled vs exact expectation), on top of the reference-pinned rows above
+# ---------------------------------------------------------------------------
+
+
+def test_cfg1_all_rows_adjoint_equals_parameter_shift(cuda):
+    circ = wl.hea_circuit(10, 4)
+    syms = circuit_symbols(circ)
+    th = wl.hea_params(1024)
+    obs = [wl.z_sum(10)]
+    e, g = ops.expectation_and_ps_gradient(circ, syms, th, obs)
+    ea, ga = ops.expectation_and_gradient(circ, syms, th, obs)
+    np.testing.assert_allclose(ea, e, atol=EXP)
+    np.testing.assert_allclose(ga, g, atol=GABS, rtol=GREL)
+
+
+def test_cfg2_all_rows_adjoint_equals_parameter_shift(cuda):
+    """All 256 headline rows: the bench's adjoint output against 400-evaluation parameter
+    shift on the same rows (the reference's gradient rule, a different code path)."""
+    circ, cost = wl.qaoa_circuit(20, 4, wl.qaoa_graph(20))
+    syms = circuit_symbols(circ)
+    th = wl.qaoa_params(256, 4)
+    e, g = ops.expectation_and_gradient([circ] * 256, syms, th, [cost])
+    ep, gp = ops.expectation_and_ps_gradient(circ, syms, th, [cost])
+    np.testing.assert_allclose(e, ep, atol=EXP)
+    np.testing.assert_allclose(g, gp, atol=GABS, rtol=GREL)
+    assert np.all(np.abs(e) <= 30.0 + 1e-3)        # |<sum of 30 ZZ>| <= 30
+
+
+def test_cfg3_rows_adjoint_equals_parameter_shift(cuda):
+    """Every 32nd of the 4096 QCNN rows (128 rows, 1080 shifted evaluations each) inside the
+    full 4096-row adjoint batch."""
+    phis, _, params = wl.qcnn_data(4096, 16)
+    model = wl.qcnn_model(16)
+    syms = circuit_symbols(model)
+    circs = [Circuit(16, list(wl.qcnn_data_circuit(p).gates) + list(model.gates)) for p in phis]
+    obs = [PauliSum([PauliString(1.0, {15: "Z"})])]
+    e, g = ops.expectation_and_gradient(circs, syms, params, obs)
+    rows = np.arange(0, 4096, 32)
+    ep, gp = ops.expectation_and_ps_gradient([circs[r] for r in rows], syms, params[rows], obs)
+    np.testing.assert_allclose(e[rows], ep, atol=EXP)
+    np.testing.assert_allclose(g[rows], gp, atol=GABS, rtol=GREL)
+    assert np.all(np.abs(e) <= 1.0 + 1e-4)
+
+
+def test_cfg4_all_circuits_norms_and_sampled_sum_z(cuda):
+    """All 64 RCS circuits: unit norms (1e-4 at 24 qubits in complex64), and the sampled
+    sum-Z (1000 shots per term) within 6 standard deviations of the exact sum-Z."""
+    import torch
+
+    circs = wl.rcs_circuits(64, 24, 20)
+    zs = wl.z_sum(24)
+    th = np.zeros((64, 0), np.float32)
+    st = ops.state(circs, [], torch.zeros((64, 0), device="cuda"))
+    norms = (st.abs() ** 2).double().sum(dim=1).cpu().numpy()
+    del st
+    np.testing.assert_allclose(norms, 1.0, atol=1e-4)
+    exact = ops.expectation(circs, [], th, [zs])[:, 0]
+    se = ops.sampled_expectation(circs, [], th, [zs], 1000,
+                                 seed=[derive_seed(wl.SEED_RCS_SHOTS + 1, i) for i in range(64)])[:, 0]
+    # per term Var(+-1) <= 1, 1000 shots, 24 independent terms
+    assert np.all(np.abs(se - exact) <= 6.0 * np.sqrt(24 / 1000.0)), np.max(np.abs(se - exact))

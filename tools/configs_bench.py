@@ -56,9 +56,15 @@ def pass_bytes(bound, grad):
     from bench import pass_bytes as pb
 
     ckpt = bool(bound.plan.extra.get("ckpt")) and grad
-    tot = sum(pb(bound.plan.fwd.prog, bound.B))
+    fb = pb(bound.plan.fwd.prog, bound.B)
+    tot = sum(fb)
     if grad:
-        tot += sum(pb(bound.plan.adj.prog, bound.B, ckpt=ckpt))
+        ab = pb(bound.plan.adj.prog, bound.B, ckpt=ckpt)
+        tot += sum(ab)
+        if ckpt and bound._turn() is not None:
+            # the turn kernel (bench.py): forward's last + backward's first pass in one launch,
+            # reading psi and writing lambda (16 B per amplitude) instead of both passes' bytes
+            tot += 16 * (1 << bound.plan.fwd.prog.n) * bound.B - fb[-1] - ab[0]
     return tot
 
 
