@@ -151,7 +151,8 @@ class DeviceProgram:
         """Plan-specialised kernels for this program (compiled on first use) or None."""
         from . import jit as _jit
 
-        if not force and not _jit.enabled(rows, self.prog.n):
+        # lane ops (warp-shuffle rotations) exist only in the plan-specialised kernels
+        if not force and not _jit.enabled(rows, self.prog.n) and not self.prog.stats.get("lane_ops"):
             return None
         if self._jit is None:
             with _JIT_LOCK:
@@ -697,7 +698,8 @@ class Engine:
         overrides = overrides or {}
         topo = pl.topology_key(template, symbol_index)
         key = (topo, obs.key, tuple(obs.diag_ids), adjoint, lam_diag, hkeys, str(device), from_state, frame,
-               tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block, jit, pl.REMAP, pl.TC_STAGES)
+               tuple(sorted(overrides.items())), pl.FUSION_ENABLED, block, jit, pl.REMAP, pl.TC_STAGES,
+               pl.LANE_OPS, pl.VEC_EDGE)
         with self._lock:
             hit = self._plans.get(key)
             if hit is not None:
@@ -766,7 +768,7 @@ class Engine:
         ckey = ("uniform", id(circuits.circuit), len(circuits)) if uniform else tuple(map(id, circuits))
         key = (ckey, symbol_names, tuple(_obs_key(o) for o in observables), bool(want_grad), str(dev),
                bool(from_state), bool(want_state), bool(norm_identity), pl.FUSION_ENABLED, pl.REMAP,
-               pl.TC_STAGES)
+               pl.TC_STAGES, pl.LANE_OPS, pl.VEC_EDGE)
         with self._lock:
             hit = self._bound.get(key)
             if hit is not None:

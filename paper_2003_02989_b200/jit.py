@@ -684,6 +684,20 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 s0, s1, moff = int(op[1]), int(op[2]), int(op[3]) - mb
                 slot = int(op[7])
                 cls, gk = int(op[9]), int(op[10])
+                if kind == pl.OP_DENSE1 and int(op[15]):
+                    # lane op: normalised X rotation on thread bit op[15] - 1 (warp shuffles)
+                    assert cls == pl.CLS_NX and int(op[15]) <= 5, (cls, int(op[15]))
+                    m = 1 << (int(op[15]) - 1)
+                    w(f"    {{ const float tau = MM[{moff}].x;")
+                    if adj and slot >= 0:
+                        assert gk == pl.GK_X and not int(op[14])
+                        sc = float(gm[int(op[8]) + 4, 0])
+                        w("      " + gs_store(slot - slb, f"{_flit(sc)} * laneGradNX<{NR}>(v0, v1, tau, {m}u)") + " }")
+                    elif adj:
+                        w(f"      laneNX2<{NR}>(v0, v1, tau, {m}u); }}")
+                    else:
+                        w(f"      laneNX<{NR}>(v0, tau, {m}u); }}")
+                    continue
                 if kind == pl.OP_DENSE1 and cls in (pl.CLS_NX, pl.CLS_NY):
                     # Pauli-frame normalised rotation: the build step wrote tau (adjoint-ready)
                     ax = 1 if cls == pl.CLS_NX else 2

@@ -63,7 +63,7 @@ INIT_LOAD, INIT_ZERO, INIT_PRODUCT, INIT_LOAD_PSI = 0, 1, 2, 3
 STAGE_INTS, OP_INTS, PASS_INTS = 64, 16, 128
 # op row: 0 kind, 1-2 register slots, 3 matrix offset, 4-6 term range / subset table, 7 slot,
 # 8 generator offset, 9 class, 10 generator kind, 11 frame x column, 12 Pauli-string code,
-# 13 block dimension, 14 merged-slot role (1 head, 2 member)
+# 13 block dimension, 14 merged-slot role (1 head, 2 member), 15 lane op: 1 + thread bit (0: none)
 # measured: two extra live accumulators push the 128-register adjoint kernels into spills
 # (SASS: +35 MOV per amplitude), so merging is off by default
 MERGE_SLOTS = __import__("os").environ.get("QF_MERGE_SLOTS", "0") not in ("0", "", "false")
@@ -524,6 +524,7 @@ def absorb_product_init(ops: list[Op], infos, n: int, allow_symbolic: bool):
 class Stage:
     regs: list            # local bits in register slots (slot j -> regs[j])
     ops: list             # Op objects in execution order
+    lane: set = field(default_factory=set)   # ids of ops applied on a lane bit (warp shuffles)
 
 
 @dataclass
@@ -700,7 +701,7 @@ def _stage_regs(need: set, R: int, L: int, lanes: set, prefer: list) -> list:
     return sorted(regs)
 
 
-def plan_stages(p: Pass, R: int, vec: bool = False) -> None:
+def plan_stages(p: Pass, R: int, vec: bool = False, lane_ok=None) -> None:
     """Register stages of one tile pass.  ``vec``: 16-byte edge accesses -- the first and
     (where its registers allow) the last stage hold local bit 0 = qubit 0 in register slot 0
     and take local bits 1..LANE_Q as lanes, so a thread loads / stores amplitude pairs
@@ -762,6 +763,28 @@ def plan_stages(p: Pass, R: int, vec: bool = False) -> None:
             raise AssertionError("stage planner made no progress")
     if not stages:
         stages.append(Stage(sorted({0} | set(range(L - R + 1, L))) if vec else list(range(L - R, L)), []))
+    if lane_ok is not None and LANE_OPS > 0 and p.out_pos is None and len(stages) >= 2:
+        # lane ops: merge the last two stages into one edge-layout stage when the gates that do
+        # not fit its registers are normalised X rotations on its first LANE_Q lane bits (the
+        # edge lanes), applied with warp shuffles -- one shared-memory exchange fewer
+        a_, b_ = stages[-2], stages[-1]
+        merged = list(a_.ops) + list(b_.ops)
+        need_r = {0} if vec else set()
+        lane_ops = []
+        for o in merged:
+            if o.kind in (OP_DIAG, OP_OBS):
+                continue
+            ls = local_set(o)
+            if len(ls) == 1 and ls <= edge_lanes and lane_ok(o):
+                lane_ops.append(o)
+            else:
+                need_r |= ls
+        if lane_ops and len(lane_ops) <= LANE_OPS and not need_r & edge_lanes and len(need_r) <= R:
+            regs = _stage_regs(need_r, R, L, lanes=edge_lanes,
+                               prefer=[b for b in b_.regs + a_.regs if b not in edge_lanes])
+            stages[-2:] = [Stage(regs, merged, {id(o) for o in lane_ops})]
+            p.stages = stages
+            return
     if vec:
         # 16-byte stores from the last stage when its ops leave local bit 0 a register slot
         # and keep off the lanes 1..LANE_Q (else the 8-byte store rule below)
@@ -822,6 +845,12 @@ CONFLICT_FREE_LANES = __import__("os").environ.get("QF_LANE_ORDER", "1") not in 
 # cfg4 22 -> 14 passes but 162 -> 186 ms -- dense brickwork passes are FMA-bound (217 fused
 # blocks x 8 FFMA2 per amplitude = 0.40 s floor at 32 qubits), so fewer HBM passes buy little
 # and the extra store stages cost more; off by default
+# lane ops (plan_stages ``lane_ok``): at most this many warp-shuffle rotations in a pass's
+# merged last stage (0: off).  Measured on the headline (one B200): one register stage and one
+# shared-memory exchange fewer per pass, but forward passes 0.746 -> 0.850 ms and backward
+# passes 2.06 -> 2.23 ms -- a lane rotation moves every amplitude's partner through SHFL (8 B
+# per amplitude and state), the exchange it replaces serves 4-9 gates; off by default
+LANE_OPS = int(__import__("os").environ.get("QF_LANE_OPS", "0"))
 # 16-byte edge loads / stores in plan-specialised kernels (plan_stages ``vec``)
 VEC_EDGE = __import__("os").environ.get("QF_VEC_EDGE", "1") not in ("0", "", "false")
 REMAP = __import__("os").environ.get("QF_REMAP", "0") not in ("0", "", "false")
@@ -1101,8 +1130,17 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
         final_pos = list(passes[-1].pos_in)
         for q, o in zip(passes[-1].qubits, passes[-1].out_pos):
             final_pos[q] = o
+    def lane_ok(op):
+        """Ops the plan-specialised kernels can apply on a lane bit: Pauli-frame normalised X
+        rotations (class CLS_NX) with, in the adjoint, a single-X generator gradient."""
+        if not (frame and op.kind == OP_DENSE1) or {infos[gi].axis for gi in op.factors} != {"X"}:
+            return False
+        if adjoint and op.symbolic:
+            return len(op.factors) == 1 and _generator_kind(infos[op.factors[0]].terms) == GK_X
+        return True
+
     for p in passes:
-        plan_stages(p, R, vec=VEC_EDGE and vec)
+        plan_stages(p, R, vec=VEC_EDGE and vec, lane_ok=lane_ok if (vec and LANE_OPS > 0) else None)
     if obs_ops:
         passes[-1].stages[-1].ops.extend(obs_ops)
     if adjoint and lam_diag:
@@ -1197,7 +1235,13 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
                 orow[8] = -1
                 orow[11] = -1
                 if op.kind in (OP_DENSE1, OP_DENSE2):
-                    if op.kind == OP_DENSE1:
+                    if op.kind == OP_DENSE1 and id(op) in st.lane:
+                        # lane op: thread bit (orow[15] - 1) of this stage's layout, no register slot
+                        order = (op.qubits[0],)
+                        orow[1] = -1
+                        orow[15] = 1 + thr.index(p.qubits.index(op.qubits[0]))
+                        assert orow[15] <= 5
+                    elif op.kind == OP_DENSE1:
                         order = (op.qubits[0],)
                         orow[1] = slot_of[op.qubits[0]]
                     else:
@@ -1382,7 +1426,8 @@ def build_program(circuit_template, infos: list[GateInfo], n: int, adjoint: bool
     stats = dict(passes=len(passes), stages=len(em.stage_rows), ops=len(em.op_rows), remapped=bool(remap),
                  stages_per_pass=[len(p.stages) for p in passes],
                  ops_per_pass=[len(p.ops) for p in passes], product_init=len(init),
-                 tile_qubits=[p.qubits for p in passes])
+                 tile_qubits=[p.qubits for p in passes],
+                 lane_ops=sum(len(st.lane) for p in passes for st in p.stages))
     return Program(
         n=n, L=L, R=R, adjoint=adjoint,
         passes=np.array(em.pass_rows, dtype=np.int32).reshape(-1, PASS_INTS),

@@ -81,6 +81,11 @@ def _chi(idx, mask):
     return 1.0 - 2.0 * par
 
 
+def _q1(o, st, reg_glob):
+    """Physical qubit of a one-qubit op: its register slot, or (lane op) its thread bit."""
+    return int(st[8 + o[15] - 1]) if o[15] else reg_glob[o[1]]
+
+
 def check_invariants(prog: pl.Program):
     R = prog.R
     for p in prog.passes:
@@ -89,8 +94,10 @@ def check_invariants(prog: pl.Program):
             st = prog.stages[si]
             reg_glob = list(st[0:R])
             lanes = list(st[8:12])
+            vec = int(st[0]) == 0       # 16-byte edge layout: qubit 0 in register slot 0
+            edge = [1, 2, 3, 4] if vec else [0, 1, 2, 3]
             if si == sb:
-                assert lanes == [0, 1, 2, 3], (si, lanes)
+                assert lanes == edge, (si, lanes)
             if si == se - 1:
                 if p[126]:   # relabelled: the store lanes are the bits stored to physical 0..3
                     outer = set(int(x) for x in p[16:16 + p[10]])
@@ -98,10 +105,12 @@ def check_invariants(prog: pl.Program):
                     out_of = {tileq[i]: int(p[84 + i]) for i in range(len(tileq))}
                     assert [out_of[int(x)] for x in lanes] == [0, 1, 2, 3], (si, lanes)
                 else:
-                    assert lanes == [0, 1, 2, 3], (si, lanes)
+                    assert lanes == edge, (si, lanes)
             for o in prog.ops[st[48]:st[49]]:
                 if o[0] == pl.OP_DENSE2:
                     assert 0 <= o[1] < o[2] < R
+                if o[0] == pl.OP_DENSE1:
+                    assert (o[1] == -1 and 1 <= o[15] <= 5) if o[15] else 0 <= o[1] < R
                 if o[0] in (pl.OP_DIAG, pl.OP_OBS):
                     g = prog.grp[o[6]: o[6] + (1 << R) + 1]
                     for S in range(1 << R):
@@ -131,7 +140,7 @@ def run_forward(prog: pl.Program, mats, angs, B, n, coefs=None, init_state=None)
                 reg_glob = list(st[0:prog.R])
                 for o in prog.ops[st[48]:st[49]]:
                     if o[0] == pl.OP_DENSE1:
-                        psi[b] = _apply(psi[b], mats[b, o[3]:o[3] + 4].reshape(2, 2), [reg_glob[o[1]]], n)
+                        psi[b] = _apply(psi[b], mats[b, o[3]:o[3] + 4].reshape(2, 2), [_q1(o, st, reg_glob)], n)
                     elif o[0] == pl.OP_DENSE2:
                         psi[b] = _apply(psi[b], mats[b, o[3]:o[3] + 16].reshape(4, 4),
                                         [reg_glob[o[1]], reg_glob[o[2]]], n)
@@ -189,7 +198,7 @@ def run_adjoint(prog: pl.Program, mats, angs, B, n, psi, lam, hcoefs):
                 reg_glob = list(st[0:prog.R])
                 for o in prog.ops[st[48]:st[49]]:
                     if o[0] in (pl.OP_DENSE1, pl.OP_DENSE2):
-                        qs = [reg_glob[o[1]]] if o[0] == pl.OP_DENSE1 else [reg_glob[o[1]], reg_glob[o[2]]]
+                        qs = [_q1(o, st, reg_glob)] if o[0] == pl.OP_DENSE1 else [reg_glob[o[1]], reg_glob[o[2]]]
                         d = 1 << len(qs)
                         u = mats[b, o[3]:o[3] + d * d].reshape(d, d)
                         if o[13]:   # fused block: U^dag, then the two-point matrix A (slots)

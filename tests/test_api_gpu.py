@@ -328,3 +328,26 @@ def test_tensor_core_stages_match_ffma2_path(cuda, monkeypatch):
     scale = float(st0.abs().max())
     assert float((st1 - st0).abs().max()) < 1e-4 * scale
     torch.testing.assert_close(e1, e0, atol=1e-4, rtol=0)
+
+
+def test_lane_op_programs_match_default(cuda, monkeypatch):
+    """Lane ops (planner.LANE_OPS, off by default: measured slower): normalised X rotations on
+    the edge layout's lane bits applied with warp shuffles (laneNX / laneGradNX), forward and
+    adjoint, equal the register-stage programs and the oracle on a QAOA batch above the
+    plan-specialised-kernel threshold."""
+    from paper_2003_02989_b200 import planner as pl
+    from paper_2003_02989_b200.engine import ENGINE
+
+    circ, cost = wl.qaoa_circuit(16, 2, wl.qaoa_graph(16, seed=2))
+    syms = circuit_symbols(circ)
+    th = wl.qaoa_params(32, 2).astype(np.float32)
+    e0, g0 = ops.expectation_and_gradient([circ] * 32, syms, th, [cost])
+    monkeypatch.setattr(pl, "LANE_OPS", 8)
+    b = ENGINE.bind([circ] * 32, syms, [cost], want_grad=True)
+    assert b.plan.fwd.prog.stats["lane_ops"] > 0 and b.plan.adj.prog.stats["lane_ops"] > 0
+    e1, g1 = ops.expectation_and_gradient([circ] * 32, syms, th, [cost])
+    np.testing.assert_allclose(e1, e0, atol=1e-5)
+    np.testing.assert_allclose(g1, g0, atol=1e-4, rtol=1e-5)
+    ee, gg = orc.adjoint_grad(circ, cost, dict(zip(syms, th[3].astype(np.float64))))
+    assert abs(e1[3, 0] - ee) < 1e-4
+    np.testing.assert_allclose(g1[3], gg, atol=1e-4, rtol=1e-5)

@@ -240,3 +240,43 @@ def test_relabelled_passes_emulated_vs_oracle(n, depth, seed, monkeypatch):
     np.testing.assert_allclose(em.logical_state(psi, prog, n)[0], ref, atol=1e-12)
     E = em.slots_to_cols(slots, prog.obs_slots, 1)[0, 0]
     assert E == pytest.approx(orc.expectation(ref, zs, n), abs=1e-10)
+
+
+def test_lane_ops_merge_last_stage(monkeypatch):
+    """Lane ops (warp-shuffle X rotations on the edge layout's lane bits): the QAOA headline's
+    forward and backward passes lose one register stage each, the ops of every pass are the
+    same, and lane ops sit on thread bits 0..3 of a pass's last planner stage only."""
+    circ, cost = wl.qaoa_circuit(20, 4, wl.qaoa_graph(20))
+    si = {s: i for i, s in enumerate(circuit_symbols(circ))}
+
+    def build(adjoint, lanes):
+        monkeypatch.setattr(pl, "LANE_OPS", lanes)
+        kw = dict(lam_diag=True) if adjoint else dict(obs_diag_ids=[0])
+        return pl.build_program(circ, pl.analyse(circ, si), 20, adjoint=adjoint, observables=[cost], frame=True,
+                                jit=True, **kw)
+
+    def pass_ops(prog):
+        out = []
+        for p in prog.passes:
+            qs = []
+            for s_ in range(p[0], p[1]):
+                st = prog.stages[s_]
+                for o in prog.ops[st[48]:st[49]]:
+                    if o[0] == pl.OP_DENSE1:
+                        qs.append(int(st[8 + o[15] - 1]) if o[15] else int(st[o[1]]))
+            out.append(sorted(qs))
+        return out
+
+    for adjoint in (False, True):
+        plain, lane = build(adjoint, 0), build(adjoint, 8)
+        em.check_invariants(lane)
+        assert plain.stats["lane_ops"] == 0 and lane.stats["lane_ops"] > 0
+        assert sum(lane.stats["stages_per_pass"]) < sum(plain.stats["stages_per_pass"])
+        assert pass_ops(lane) == pass_ops(plain)
+        for p in lane.passes:
+            edge = p[1] - 1 if not adjoint else p[0]      # the planner's last stage
+            for s_ in range(p[0], p[1]):
+                st = lane.stages[s_]
+                for o in lane.ops[st[48]:st[49]]:
+                    if o[15]:
+                        assert s_ == edge and 1 <= o[15] <= 4 and o[9] == pl.CLS_NX
