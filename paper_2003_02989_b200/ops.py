@@ -59,6 +59,20 @@ def _out(t, on_dev):
     return t if on_dev else t.cpu().numpy()
 
 
+def _outs(ts, on_dev):
+    """Several device results to the host with ONE stream synchronisation: asynchronous
+    copies into pinned buffers (torch's caching host allocator), then a single sync."""
+    if on_dev:
+        return tuple(ts)
+    if not all(t.is_cuda and t.device == ts[0].device for t in ts) or len(devices()) > 1:
+        return tuple(t.cpu().numpy() for t in ts)
+    hs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in ts]
+    for h, t in zip(hs, ts):
+        h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(ts[0].device).synchronize()
+    return tuple(h.numpy() for h in hs)
+
+
 # ---------------------------------------------------------------------------
 # row partitioning: one launch sequence per (topology, device)
 # ---------------------------------------------------------------------------
@@ -212,7 +226,7 @@ def expectation_and_gradient(circuits, symbol_names, symbol_values, operators, u
         return np.zeros((0, len(ops))), np.zeros((0, len(symbol_names)))
     out = _run(circuits, symbol_names, vals, ops, want_grad=True, upstream=upstream,
                keys=("expectations", "grad"))
-    return _out(out["expectations"], on_dev), _out(out["grad"], on_dev)
+    return _outs((out["expectations"], out["grad"]), on_dev)
 
 
 def expectation_and_ps_gradient(circuits, symbol_names, symbol_values, operators, upstream=None,

@@ -338,14 +338,17 @@ def test_lane_op_programs_match_default(cuda, monkeypatch):
     from paper_2003_02989_b200 import planner as pl
     from paper_2003_02989_b200.engine import ENGINE
 
+    # 256 rows x 2^16 amplitudes: at the Pauli-frame size threshold (engine FRAME_MIN_AMPS), so the
+    # mixer rotations are normalised X rotations -- the ops lane ops apply
+    B = 256
     circ, cost = wl.qaoa_circuit(16, 2, wl.qaoa_graph(16, seed=2))
     syms = circuit_symbols(circ)
-    th = wl.qaoa_params(32, 2).astype(np.float32)
-    e0, g0 = ops.expectation_and_gradient([circ] * 32, syms, th, [cost])
+    th = wl.qaoa_params(B, 2).astype(np.float32)
+    e0, g0 = ops.expectation_and_gradient([circ] * B, syms, th, [cost])
     monkeypatch.setattr(pl, "LANE_OPS", 8)
-    b = ENGINE.bind([circ] * 32, syms, [cost], want_grad=True)
+    b = ENGINE.bind([circ] * B, syms, [cost], want_grad=True)
     assert b.plan.fwd.prog.stats["lane_ops"] > 0 and b.plan.adj.prog.stats["lane_ops"] > 0
-    e1, g1 = ops.expectation_and_gradient([circ] * 32, syms, th, [cost])
+    e1, g1 = ops.expectation_and_gradient([circ] * B, syms, th, [cost])
     np.testing.assert_allclose(e1, e0, atol=1e-5)
     np.testing.assert_allclose(g1, g0, atol=1e-4, rtol=1e-5)
     ee, gg = orc.adjoint_grad(circ, cost, dict(zip(syms, th[3].astype(np.float64))))
