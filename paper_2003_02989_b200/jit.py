@@ -344,6 +344,11 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     st += " " + gs_flush(slot_rel - (RING - 1), RING)
                 return st
             return f"{{ const float gsv = warp_sum_f({expr}); if ((t & 31u) == 0u) GS[{slot_rel * GSW} + (t >> 5)] = gsv; }}"
+        pad = int(os.environ.get("QF_SMEM_PAD_ADJ" if adj else "QF_SMEM_PAD_FWD", "0"))
+        if pad:
+            # experiment: dynamic shared memory padded to limit the CTAs per SM (instruction-cache
+            # pressure of long straight-line passes vs occupancy)
+            smem = max(smem, pad)
         geo.append((NT, smem))
         o = []
         w = o.append
@@ -435,13 +440,18 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             w(f"  {{ const float2* __restrict__ src = a.mats + (size_t)row * a.n_mat + {mb};")
             w(f"    for (int i = t; i < {mcnt}; i += {NT}) {{ const float2 x = src[i]; MM[i] = make_float4(x.x, x.y, -x.y, x.y); }}")
             if adj:
+                # one barrier orders the straight copy before every transposed rewrite (the
+                # rewrites of different ops touch disjoint entries)
+                first_t = True
                 for op_ in pass_ops:
                     kd, cl_ = int(op_[0]), int(op_[9])
                     if kd not in (pl.OP_DENSE1, pl.OP_DENSE2) or cl_ in (pl.CLS_NX, pl.CLS_NY):
                         continue
                     D = 2 if kd == pl.OP_DENSE1 else 4
                     off = int(op_[3]) - mb
-                    w(f"    __syncthreads();")
+                    if first_t:
+                        w(f"    __syncthreads();")
+                        first_t = False
                     w(f"    if (t < {D * D}) {{ const float2 x = src[{off} + (t % {D}) * {D} + t / {D}];"
                       f" MM[{off} + t] = make_float4(x.x, -x.y, x.y, -x.y); }}")
             w("  }")
