@@ -290,6 +290,30 @@ def pass_bytes(prog, rows, ckpt=False):
     return out
 
 
+def _rank_device(torch):
+    """One GPU per rank (LOCAL_RANK); QF_BENCH_DEVICE pins every rank to one device (the GPU
+    tests run two gloo ranks on the one-GPU box: their kernels never wait on each other)."""
+    local = int(os.environ.get("QF_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
+    torch.cuda.set_device(local)
+    return local, torch.device("cuda", local)
+
+
+def _init_group(dist, args, dev):
+    backend = args.backend or "nccl"
+    if backend == "nccl":
+        dist.init_process_group(backend, device_id=dev)
+    else:
+        dist.init_process_group(backend)
+
+
+def _max_over_ranks(torch, dist, x: float, dev) -> float:
+    """Max of a per-rank time over all ranks (on the device for NCCL, on the host for gloo)."""
+    on_host = dist.get_backend() == "gloo"
+    t = torch.tensor([x], device="cpu" if on_host else dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_gpu(args, rank, world):
     import ctypes as C
 
@@ -301,11 +325,9 @@ def run_gpu(args, rank, world):
     from paper_2003_02989_b200 import workloads as wl
     from paper_2003_02989_b200.engine import ENGINE, _ptr
 
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    local, dev = _rank_device(torch)
     if world > 1:
-        dist.init_process_group(args.backend or "nccl", device_id=dev)
+        _init_group(dist, args, dev)
     circ, cost, syms = workload()
     theta_np = wl.qaoa_params(BATCH * world, DEPTH)[rank * BATCH:(rank + 1) * BATCH]
     theta = torch.as_tensor(theta_np).to(dev)
@@ -336,9 +358,7 @@ def run_gpu(args, rank, world):
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks(torch, dist, ms, dev)
     value = BATCH * world / (ms / 1000.0)
 
     # ---- per-launch profile of the tile-pass kernels (roofline) ----
@@ -462,9 +482,7 @@ def run_gpu(args, rank, world):
     barrier()
     e2e_ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = _max_over_ranks(torch, dist, e2e_ms, dev)
     e2e = BATCH * world / (e2e_ms / 1000.0)
 
     # ---- the same 256 rows with the reference's gradient rule (parameter shift) on the GPU:
@@ -541,11 +559,9 @@ def run_big32(args, rank, world):
     g = world.bit_length() - 1
     if world != 1 << g or g > 3:
         raise SystemExit(f"big32 needs 1, 2, 4 or 8 ranks, got {world}")
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    local, dev = _rank_device(torch)
     if world > 1:
-        dist.init_process_group(args.backend or "nccl", device_id=dev)
+        _init_group(dist, args, dev)
     circ = wl.brickwork_circuit(n, 14, wl.SEED_BIG)
     obs = wl.z_sum(n)
     stream = torch.cuda.current_stream(dev)
@@ -586,9 +602,7 @@ def run_big32(args, rank, world):
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks(torch, dist, ms, dev)
     e = float(res if not isinstance(res, torch.Tensor) else res.reshape(-1)[0])
     if rank == 0:
         peak, peak_kind = _peaks()

@@ -96,3 +96,34 @@ def test_engine_global_qubit_sharding_two_ranks(cuda, tmp_path):
     want = float(ops.expectation(c, [], np.zeros((1, 0), np.float32), [wl.z_sum(n)])[0, 0])
     assert swaps >= 1
     assert e == pytest.approx(want, abs=1e-5)
+
+
+def _bench(args, env_extra):
+    env = dict(os.environ, QF_BENCH_DEVICE="0", MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS="1", **env_extra)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    import json
+
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_bench_launcher_two_ranks_on_gpu():
+    """bench.py --gpus 2 starts its own two ranks (torch.distributed.run); both run the headline
+    step on the GPU (gloo group, QF_BENCH_DEVICE pins them to the one device) and rank 0 prints
+    the max-over-ranks line for the whole 512-row job."""
+    d = _bench(["--gpus", "2", "--backend", "gloo", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-ps"], {})
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 512 and d["value"] > 0
+    assert d["e2e"]["value"] > 0 and d["scaling"] == "weak"
+
+
+def test_bench_big32_two_ranks_on_gpu():
+    """bench.py --workload big32 at 24 qubits: 2 ranks (one global qubit, gloo all-to-all of the
+    shards through host memory) give the single-rank expectation."""
+    one = _bench(["--workload", "big32", "--steps", "2", "--warmup", "3"], {"QF_BIG_QUBITS": "24"})
+    two = _bench(["--workload", "big32", "--gpus", "2", "--backend", "gloo", "--steps", "2", "--warmup", "3"],
+                 {"QF_BIG_QUBITS": "24"})
+    assert two["n_gpus"] == 2 and two["config"]["global_qubits"] == 1 and two["config"]["swaps"] >= 1
+    assert two["expectation"] == pytest.approx(one["expectation"], abs=1e-5)
