@@ -67,6 +67,8 @@ L2PF = int(os.environ.get("QF_L2PF", "0") or 0)
 # a barrier before each inner exchange's writes (not needed: see generate)
 PREW_SYNC = os.environ.get("QF_PREW_SYNC", "0") not in ("0", "", "false")
 SPLIT_XCHG = os.environ.get("QF_SPLIT_XCHG", "0") not in ("0", "", "false")
+# exchange addresses as (tp ^ low nibble) + high bits (immediate offsets; _sm_idx)
+XADD = os.environ.get("QF_XADD", "1") not in ("0", "", "false")
 SPLIT_LIGHT_OPS = int(os.environ.get("QF_SPLIT_LIGHT_OPS", "12"))
 ADJ3 = os.environ.get("QF_ADJ3", "0") not in ("0", "", "false")
 L2PF_SMS = int(os.environ.get("QF_L2PF_SMS", "148"))
@@ -80,6 +82,18 @@ STREAM_POLY = os.environ.get("QF_STREAM_POLY", "auto")   # auto: R >= 5 (measure
 
 def _flit(x: float) -> str:
     return repr(float(np.float32(x))) + "f"
+
+
+def _sm_idx(c: int) -> str:
+    """Shared-memory index tp ^ c of an exchange.  Under planner.swizzle the thread part and the
+    register part share only the low nibble (bits >= 4 are distinct local bits), so
+    tp ^ c = (tp ^ (c & 15)) + (c & ~15): one XOR per distinct low nibble (common
+    subexpression across registers), the rest an immediate LDS/STS offset."""
+    lo, hi = c & 15, c & ~15
+    if not XADD:
+        return f"(tp ^ {c}u)"
+    base = f"(tp ^ {lo}u)" if lo else "tp"
+    return f"({base} + {hi}u)" if hi else base
 
 
 def _xor_expr(bits: list, var: str = "t") -> str:
@@ -631,26 +645,26 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                             w("  __syncthreads();")
                         w(f"  {{ const u32 tp = {_xor_expr(tphys(prev))};")
                         for r in range(NR):
-                            w(f"    sm[tp ^ {roff(prev, r, True)}u] = {vv}[{r}];")
+                            w(f"    sm[{_sm_idx(roff(prev, r, True))}] = {vv}[{r}];")
                         w("  }")
                         w("  __syncthreads();")
                         w(f"  {{ const u32 tp = {_xor_expr(tphys(st))};")
                         for r in range(NR):
-                            w(f"    {vv}[{r}] = sm[tp ^ {roff(st, r, True)}u];")
+                            w(f"    {vv}[{r}] = sm[{_sm_idx(roff(st, r, True))}];")
                         w("  }")
                 else:
                     w(f"  {{ const u32 tp = {_xor_expr(tphys(prev))};")
                     for r in range(NR):
-                        w(f"    sm[tp ^ {roff(prev, r, True)}u] = v0[{r}];")
+                        w(f"    sm[{_sm_idx(roff(prev, r, True))}] = v0[{r}];")
                         if adj:
-                            w(f"    sm[{TILE} + (tp ^ {roff(prev, r, True)}u)] = v1[{r}];")
+                            w(f"    sm[{TILE} + {_sm_idx(roff(prev, r, True))}] = v1[{r}];")
                     w("  }")
                     w("  __syncthreads();")
                     w(f"  {{ const u32 tp = {_xor_expr(tphys(st))};")
                     for r in range(NR):
-                        w(f"    v0[{r}] = sm[tp ^ {roff(st, r, True)}u];")
+                        w(f"    v0[{r}] = sm[{_sm_idx(roff(st, r, True))}];")
                         if adj:
-                            w(f"    v1[{r}] = sm[{TILE} + (tp ^ {roff(st, r, True)}u)];")
+                            w(f"    v1[{r}] = sm[{TILE} + {_sm_idx(roff(st, r, True))}];")
                     w("  }")
             reg_glob = [int(st[j]) for j in range(R)]
             need_gt = any(int(prog.ops[k][0]) in (pl.OP_DIAG, pl.OP_OBS) for k in range(int(st[48]), int(st[49])))
@@ -1164,11 +1178,11 @@ def generate_turn(fwd: pl.Program, adj: pl.Program, name: str = "qf_turn") -> tu
             return x
         o.append("  { float2* sm = reinterpret_cast<float2*>(smem_raw); const u32 t = threadIdx.x;")
         o.append(f"    {{ const u32 tp = {tp(sf)};")
-        o += [f"      sm[tp ^ {ro(sf, r)}u] = v0[{r}];" for r in range(NR)]
+        o += [f"      sm[{_sm_idx(ro(sf, r))}] = v0[{r}];" for r in range(NR)]
         o.append("    }")
         o.append("    __syncthreads();")
         o.append(f"    {{ const u32 tp = {tp(sa)};")
-        o += [f"      v0[{r}] = sm[tp ^ {ro(sa, r)}u];" for r in range(NR)]
+        o += [f"      v0[{r}] = sm[{_sm_idx(ro(sa, r))}];" for r in range(NR)]
         o.append("    }")
         o.append("    __syncthreads();")
         o.append("  }")
