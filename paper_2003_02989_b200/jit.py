@@ -69,7 +69,7 @@ PREW_SYNC = os.environ.get("QF_PREW_SYNC", "0") not in ("0", "", "false")
 SPLIT_XCHG = os.environ.get("QF_SPLIT_XCHG", "0") not in ("0", "", "false")
 # exchange addresses as (tp ^ low nibble) + high bits (immediate offsets; _sm_idx)
 XADD = os.environ.get("QF_XADD", "1") not in ("0", "", "false")
-SPLIT_LIGHT_OPS = int(os.environ.get("QF_SPLIT_LIGHT_OPS", "12"))
+SPLIT_LIGHT_OPS = int(os.environ.get("QF_SPLIT_LIGHT_OPS", "64"))
 ADJ3 = os.environ.get("QF_ADJ3", "0") not in ("0", "", "false")
 L2PF_SMS = int(os.environ.get("QF_L2PF_SMS", "148"))
 # integer-weight phase polynomials evaluated per amplitude in Gray-code order (one live value)
@@ -272,10 +272,11 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         GSW = NT if (per_thread_gs or chunked) else NT // 32
         ws_floats = (NT // 32) * 32 if (scnt and (per_thread_gs or chunked)) else 0
         gs_slots = min(scnt, RING) if chunked else scnt
-        # light backward passes of the R = 5 rotation programs (the turn kernel's backward part,
-        # the last backward pass): psi and lambda exchanged one after the other through one tile
-        # buffer, 3 CTAs/SM (measured on the headline: turn 1.40 -> 1.29 ms, last pass 1.33 ->
-        # 1.31 ms; the 20-op middle passes spill at 168 registers and lose, 2.07 -> 2.26 ms)
+        # backward passes of the R = 5 rotation programs with at most SPLIT_LIGHT_OPS gate ops
+        # (default: all): psi and lambda exchanged one after the other through one tile buffer,
+        # 3 CTAs/SM at 168 registers.  Measured on the headline: turn 1.40 -> 1.29 ms, last pass
+        # 1.33 -> 1.31 ms; the 20-op middle passes first spilled (2.07 -> 2.26 ms), and with the
+        # immediate-offset exchange addresses (_sm_idx: no spills) gain, 2.07 -> 1.99 ms
         light = (adj and R == 5 and L == 12 and not env_minb and SPLIT_LIGHT_OPS > 0 and not PERSIST
                  and n_gate_ops <= SPLIT_LIGHT_OPS)
         NX = 1 if (adj and (SPLIT_XCHG or light)) else NA
