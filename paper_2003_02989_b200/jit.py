@@ -69,6 +69,7 @@ PREW_SYNC = os.environ.get("QF_PREW_SYNC", "0") not in ("0", "", "false")
 SPLIT_XCHG = os.environ.get("QF_SPLIT_XCHG", "0") not in ("0", "", "false")
 # exchange addresses as (tp ^ low nibble) + high bits (immediate offsets; _sm_idx)
 XADD = os.environ.get("QF_XADD", "1") not in ("0", "", "false")
+ADJ_LOADS_FIRST = os.environ.get("QF_ADJ_LOADS_FIRST", "auto")   # "0", "1" or "auto" (heavy passes)
 SPLIT_LIGHT_OPS = int(os.environ.get("QF_SPLIT_LIGHT_OPS", "64"))
 ADJ3 = os.environ.get("QF_ADJ3", "0") not in ("0", "", "false")
 L2PF_SMS = int(os.environ.get("QF_L2PF_SMS", "148"))
@@ -622,8 +623,10 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 w("    }")
                 w("  }")
         mark_load_end = len(o)
-        if not PERSIST and not prefetch and not adj and init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI):
-            # (forward sweep only: measured slower for the adjoint)
+        loads_first = (not adj) or (ADJ_LOADS_FIRST == "1") or (ADJ_LOADS_FIRST == "auto" and n_gate_ops > 12)
+        if not PERSIST and not prefetch and loads_first and init in (pl.INIT_LOAD, pl.INIT_LOAD_PSI):
+            # backward passes: only the heavy ones (measured on the headline at 3 CTAs/SM: 20-op
+            # passes 1.99-2.02 -> 1.95-2.00 ms; the 8/12-op turn and last pass lose 3-5%)
             # issue the tile's global loads before staging the row's matrices / tables, so
             # the staging latency (loads, syncs, table sincos) hides behind the tile loads
             vdecl = [ln for ln in o[mark_stage:mark_ptr] if ln.startswith("  float2 v0[") or
