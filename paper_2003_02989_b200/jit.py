@@ -69,6 +69,7 @@ PREW_SYNC = os.environ.get("QF_PREW_SYNC", "0") not in ("0", "", "false")
 SPLIT_XCHG = os.environ.get("QF_SPLIT_XCHG", "0") not in ("0", "", "false")
 # exchange addresses as (tp ^ low nibble) + high bits (immediate offsets; _sm_idx)
 XADD = os.environ.get("QF_XADD", "1") not in ("0", "", "false")
+GS_RING = int(os.environ.get("QF_GS_RING", "16"))
 ADJ_LOADS_FIRST = os.environ.get("QF_ADJ_LOADS_FIRST", "auto")   # "0", "1" or "auto" (heavy passes)
 SPLIT_LIGHT_OPS = int(os.environ.get("QF_SPLIT_LIGHT_OPS", "64"))
 ADJ3 = os.environ.get("QF_ADJ3", "0") not in ("0", "", "false")
@@ -266,7 +267,9 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         # registers, slot partials in a 12-slot ring so that three CTAs' shared memory fits
         adj3 = adj and R == 5 and L == 12 and ADJ3 and not env_minb and not PERSIST and n_gate_ops > SPLIT_LIGHT_OPS
         per_thread_gs = scnt * NT * 4 <= GS_THREAD_BYTES and not (adj3 and scnt > 12)
-        RING = 12 if adj3 else 16
+        # ring of per-thread slots: 32 (flushed as two 16-value chunks under one barrier pair)
+        # or 16 (QF_GS_RING)
+        RING = 12 if adj3 else GS_RING
         # many slots: a ring of 16 per-thread slots flushed by a 16-value warp transpose-reduction
         # (slots must then be stored in slot order: not with merged accumulators)
         chunked = (not per_thread_gs) and CHUNKED_GS and NT >= 64 and not merged_last
@@ -343,6 +346,10 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             if flushes[0]:
                 code.append("__syncthreads();")
             code.append("if ((t & 16u) == 0u) WS[(t >> 5) * 32 + (t & 15u)] = x[0];")
+            if K > 16:     # second chunk: ring positions 16..K-1 into the upper half of WS
+                code += [f"x[{i}] = {f'GS[{(16 + i) * NT} + t]' if 16 + i < K else '0.f'};" for i in range(16)]
+                code.append("warp_transpose_sum16(x, t & 31u);")
+                code.append("if ((t & 16u) == 0u) WS[(t >> 5) * 32 + 16 + (t & 15u)] = x[0];")
             code.append("__syncthreads();")
             code.append(f"if (t < {K}) {{ double acc = 0.0; for (int wv = 0; wv < {NWP}; ++wv) "
                         f"acc += (double)WS[wv * 32 + t]; a.partials[((size_t)row * a.n_slots + {slb + c0} + t) * "
