@@ -335,6 +335,10 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             # is faster (QCNN forward passes 21.9 -> 20.3 ms)
             minb_p = min(minb_p, 3)
 
+        # gradient accumulation chains per rotation: 4 in the light backward passes (turn kernel
+        # 1.21 -> 1.17 ms), the prelude default (2) elsewhere
+        chains = int(os.environ.get("QF_GRAD_CHAINS_LIGHT", "4")) if (adj and light and n_gate_ops <= 12) \
+            else int(os.environ.get("QF_GRAD_CHAINS", "2"))
         flushes = [0]
 
         def gs_flush(c0, K):
@@ -765,7 +769,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                     elif adj and slot >= 0:
                         g0 = int(op[8])
                         sc = float(gm[g0 + 4, 0])
-                        w("      " + gs_store(slot - slb, f"{_flit(sc)} * gradp<{s0}, {NR}, {gk}>(v0, v1)"))
+                        w("      " + gs_store(slot - slb, f"{_flit(sc)} * gradp<{s0}, {NR}, {gk}, {chains}>(v0, v1)"))
                     if adj:
                         w(f"      applyN<{s0}, {NR}, {ax}>(v1, tau);")
                     w(f"      applyN<{s0}, {NR}, {ax}>(v0, tau); }}")
