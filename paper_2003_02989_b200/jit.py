@@ -335,10 +335,15 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
             # is faster (QCNN forward passes 21.9 -> 20.3 ms)
             minb_p = min(minb_p, 3)
 
-        # gradient accumulation chains per rotation: 4 in the light backward passes (turn kernel
-        # 1.21 -> 1.17 ms), the prelude default (2) elsewhere
-        chains = int(os.environ.get("QF_GRAD_CHAINS_LIGHT", "4")) if (adj and light and n_gate_ops <= 12) \
-            else int(os.environ.get("QF_GRAD_CHAINS", "2"))
+        # gradient accumulation chains per rotation (R = 5 backward passes at 3 CTAs/SM): 4 in the
+        # light passes (turn kernel 1.21 -> 1.17 ms), 1 in the heavy ones (fewer live registers:
+        # contiguous middle pass 1.99 -> 1.96 ms), the prelude default (2) elsewhere
+        if adj and light and n_gate_ops <= 12:
+            chains = int(os.environ.get("QF_GRAD_CHAINS_LIGHT", "4"))
+        elif adj and light:
+            chains = int(os.environ.get("QF_GRAD_CHAINS_HEAVY", "1"))
+        else:
+            chains = int(os.environ.get("QF_GRAD_CHAINS", "2"))
         flushes = [0]
 
         def gs_flush(c0, K):
