@@ -604,15 +604,18 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
                 if mo < 0:
                     w(f"  if ((gt0 >> {q}) & 1u) c = make_float2(0.f, 0.f);")
                 else:
-                    w(f"  c = cmul(c, ((gt0 >> {q}) & 1u) ? mm2(MM, {mo - mb + 2}) : mm2(MM, {mo - mb}));")
+                    w(f"  c = cmul_m(c, MM[((gt0 >> {q}) & 1u) ? {mo - mb + 2} : {mo - mb}]);")
             w("  v0[0] = c;")
             for j in range(R):
                 mo = init_mat[int(st0[j])]
-                f0 = "make_float2(1.f, 0.f)" if mo < 0 else f"mm2(MM, {mo - mb})"
-                f1 = "make_float2(0.f, 0.f)" if mo < 0 else f"mm2(MM, {mo - mb + 2})"
-                w(f"  {{ const float2 f0 = {f0}, f1 = {f1};")
-                for r in range(1 << j):
-                    w(f"    v0[{r | (1 << j)}] = cmul(v0[{r}], f1); v0[{r}] = cmul(v0[{r}], f0);")
+                if mo < 0:
+                    w(f"  {{ const float2 f0 = make_float2(1.f, 0.f), f1 = make_float2(0.f, 0.f);")
+                    for r in range(1 << j):
+                        w(f"    v0[{r | (1 << j)}] = cmul(v0[{r}], f1); v0[{r}] = cmul(v0[{r}], f0);")
+                else:
+                    w(f"  {{ const float4 f0 = MM[{mo - mb}], f1 = MM[{mo - mb + 2}];")
+                    for r in range(1 << j):
+                        w(f"    v0[{r | (1 << j)}] = cmul_m(v0[{r}], f1); v0[{r}] = cmul_m(v0[{r}], f0);")
                 w("  }")
 
         if (L2PF >= (1 if adj else 2) and not PERSIST and fuse != "tail" and EXP_MODE != "noload"
