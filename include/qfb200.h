@@ -274,6 +274,14 @@ int qf_jit_function(void* module, const char* name, int max_dyn_smem, void** fun
 int qf_jit_unload(void* module);
 /* Resident CTAs per SM of a loaded pass kernel (grid size of the persistent kernels). */
 int qf_jit_occupancy(void* func, int block, int dyn_smem, int* blocks_per_sm);
+/* Device address / size of a loaded module's __constant__ symbol (jit.py constant slabs). */
+int qf_jit_global(void* module, const char* name, void** dptr, size_t* bytes);
+/* Stage one pass's rotation coefficients into its module's constant slab on `stream`:
+ * staging[row][j] = (x, x), x = Re mats[row * n_mat + cols[j]], then a device copy into
+ * `symbol` (rows * k * 8 bytes <= symbol_bytes).  Replaces nothing in the reference (the
+ * reference has no native code; this feeds the kernels that replace qcflow sim.py:88-105). */
+int qf_jit_cm_stage(const void* mats, int n_mat, int rows, const int* cols, int k, void* staging, void* symbol,
+                    size_t symbol_bytes, void* stream);
 /* Launch n generated pass kernels in order on `stream` with one packed argument struct
  * (QfJitArgs in csrc/qf_jit_prelude.cuh). */
 int qf_jit_run(void* const* funcs, const uint32_t* grid, const uint32_t* block, const uint32_t* smem, int n,

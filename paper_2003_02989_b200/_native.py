@@ -19,7 +19,7 @@ EXPORTS = (
     "qf_jit_compile", "qf_jit_free", "qf_jit_load", "qf_jit_function", "qf_jit_unload", "qf_jit_run",
     "qf_reduce_slots_scaled", "qf_frame_walk", "qf_jit_occupancy", "qf_frame_walk_ckpt", "qf_block_grads",
     "qf_sample_multi", "qf_reduce_slots_offset", "qf_permute_bits", "qf_dense4_tc_prepare", "qf_dense4_tc",
-    "qf_tc_build",
+    "qf_tc_build", "qf_jit_global", "qf_jit_cm_stage",
 )
 
 _p = C.c_void_p
@@ -101,6 +101,8 @@ def load(build_if_missing: bool = True):
     lib.qf_jit_unload.argtypes = [_p]
     lib.qf_jit_occupancy.argtypes = [_p, C.c_int, C.c_int, C.POINTER(C.c_int)]
     lib.qf_jit_run.argtypes = [_p, _p, _p, _p, C.c_int, _p, _p, C.c_size_t]
+    lib.qf_jit_global.argtypes = [_p, C.c_char_p, C.POINTER(_p), C.POINTER(C.c_size_t)]
+    lib.qf_jit_cm_stage.argtypes = [_p, C.c_int, C.c_int, _p, C.c_int, _p, _p, C.c_size_t, _p]
     for name in EXPORTS:
         getattr(lib, name).restype = C.c_int if name != "qf_last_error" else C.c_char_p
     lib.qf_jit_free.restype = None

@@ -97,6 +97,7 @@ class DeviceProgram:
         self.n_terms = len(r["term_beta"])
         self.tiles = 1 << (prog.n - prog.L)
         self._jit = None
+        self._jit_cm = None
         self.frame = bool(prog.frame)
         ev = prog.frame_events if prog.frame_events is not None else np.zeros((0, pl.EV_INTS), np.int32)
         self.n_events = int(ev.shape[0])
@@ -154,6 +155,16 @@ class DeviceProgram:
         # lane ops (warp-shuffle rotations) exist only in the plan-specialised kernels
         if not force and not _jit.enabled(rows, self.prog.n) and not self.prog.stats.get("lane_ops"):
             return None
+        if self._jit_cm is None and _jit.CTAU and self.prog.adjoint:
+            # adjoint programs: rotation coefficients from constant slabs (jit.CTAU) when the
+            # launch's rows fit them; other row counts take the shared-memory variant
+            with _JIT_LOCK:
+                if self._jit_cm is None:
+                    self._jit_cm = _jit.JitProgram(self.prog, device.index or 0, cm=True)
+        if self._jit_cm is not None and self._jit_cm.cm and rows <= self._jit_cm.cm_rows_max:
+            return self._jit_cm
+        if self._jit_cm is not None and not self._jit_cm.cm:
+            return self._jit_cm     # no rotation coefficients: the same kernels
         if self._jit is None:
             with _JIT_LOCK:
                 if self._jit is None:
@@ -403,7 +414,9 @@ class Bound:
                     self._execute(static, want_grad=want_grad, want_expect=want_expect)
                 cur.wait_stream(side)
                 graph = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                # captured on the warm-up stream: its per-stream kernel modules (constant slabs,
+                # jit.CTAU) are loaded already and belong to this graph alone
+                with torch.cuda.graph(graph, stream=side, capture_error_mode="thread_local"):
                     out = self._execute(static, want_grad=want_grad, want_expect=want_expect)
                 hit = (self, graph, static, out)
                 _GRAPHS[key] = hit

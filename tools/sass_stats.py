@@ -62,7 +62,7 @@ def programs(name):
 def stats(src, name, keep):
     cu = os.path.join(keep, name + ".cu")
     with open(cu, "w") as f:
-        f.write(jit.prelude() + "\n" + src)
+        f.write(jit.full_source(src))
     cub = cu.replace(".cu", ".cubin")
     r = subprocess.run(["nvcc", "-cubin", "-arch=sm_100a", "-std=c++17", "-O3", "-Xptxas", "-v", cu, "-o", cub],
                        capture_output=True, text=True)
