@@ -513,7 +513,9 @@ def run_gpu(args, rank, world):
         # per step: passes + 2 builds (qf_build_ops: dense + angle kernels each) + 2 frame
         # walks + 3 slot reductions (expectation, gradient, energy); no ATen kernels remain in
         # the step (cross-checked against the ncu launch list under profiles/)
-        n_launch = len(launches) + 4 + (2 if fw.frame else 0) + 3
+        # + one coefficient gather (qf_jit_cm_stage) per backward pass with a constant slab
+        n_gather = sum(1 for i in range(1 if turn else 0, ja.n) if ja.cm and ja.cm_k[i]) if ja is not None else 0
+        n_launch = len(launches) + 4 + (2 if fw.frame else 0) + 3 + n_gather
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -393,7 +393,7 @@ def generate(prog: pl.Program, tag: str, remote_pass: int = -1, remote_g: int = 
         geo.append((NT, smem))
         o = []
         w = o.append
-        use_cm = cm and adj and fuse is None
+        use_cm = cm and adj and fuse in (None, "tail")
         cm_slots = {}    # staged-slab offset of a rotation coefficient -> its column in qf_cm
 
         def tau_ref(moff_, pair=False):
@@ -1184,14 +1184,18 @@ def _turn_compatible(fwd: pl.Program, adj: pl.Program) -> bool:
     return outer_f == outer_a and int(pa[2]) == pl.INIT_LOAD_PSI and not int(pf[126])
 
 
-def generate_turn(fwd: pl.Program, adj: pl.Program, name: str = "qf_turn") -> tuple[str, int, int]:
+def generate_turn(fwd: pl.Program, adj: pl.Program, name: str = "qf_turn", cm: bool = False) -> tuple[str, int, int]:
     """One kernel for the forward's last tile pass and the backward's first (checkpointed,
     lambda = H psi fused): the final state never leaves registers -- no store of it by the
     forward, no load of it by the backward.  Parameters (forward args ``a``, backward args
     ``b``).  Returns (source, threads per CTA, dynamic smem bytes)."""
     P = len(fwd.passes)
     fs, _, fg = generate(fwd, "f", fuse="head", only_pass=P - 1)
-    bs, _, bg = generate(adj, "a", fuse="tail", only_pass=0)
+    bs, _, bg = generate(adj, "a", fuse="tail", only_pass=0, cm=cm)
+    prefix = ""
+    if bs[0].startswith("// QF_CM_COLS "):       # the backward half's constant slab
+        head, decl, rest = bs[0].split("\n", 2)
+        prefix, bs = head + "\n" + decl + "\n", [rest]
     NT, NR = fg[0][0], 1 << fwd.R
     assert bg[0][0] == NT
     import re
@@ -1238,7 +1242,7 @@ def generate_turn(fwd: pl.Program, adj: pl.Program, name: str = "qf_turn") -> tu
         o.append("    __syncthreads();")
         o.append("  }")
     o += ["  {"] + ab + ["  }", "}"]
-    return "\n".join(o) + "\n", NT, max(fg[0][1], bg[0][1])
+    return prefix + "\n".join(o) + "\n", NT, max(fg[0][1], bg[0][1])
 
 
 class QfTurnArgs(C.Structure):
@@ -1248,9 +1252,13 @@ class QfTurnArgs(C.Structure):
 class TurnKernel:
     """The compiled turn kernel of one (forward, backward) program pair."""
 
-    def __init__(self, fwd: pl.Program, adj: pl.Program, device_index: int):
+    def __init__(self, fwd: pl.Program, adj: pl.Program, device_index: int, cm: bool = None):
         lib = nat.load()
-        src, self.nt, self.smem = generate_turn(fwd, adj)
+        if cm is None:
+            # measured: no gain on the headline's turn kernel (1.1654 vs 1.1656 ms; its FFMA2s
+            # are mostly the forward half's), so off by default
+            cm = CTAU and os.environ.get("QF_CTAU_TURN", "0") not in ("0", "", "false")
+        src, self.nt, self.smem = generate_turn(fwd, adj, cm=cm)
         img = compile_kernel(src, "qf_turn")
         self.module = C.c_void_p()
         nat.check(lib.qf_jit_load(img, C.byref(self.module)))
@@ -1259,6 +1267,12 @@ class TurnKernel:
         self.func = (C.c_void_p * 1)(f.value)
         self.fwd, self.adj = fwd, adj
         self.rows_shift = fwd.n - fwd.L
+        self.device_index = device_index
+        self._slabs, self._plain = None, None
+        if src.startswith("// QF_CM_COLS "):
+            cols = [int(x) for x in src.split("\n", 1)[0].split()[2].split(",")]
+            self._slabs = _SlabModules([img], ["qf_turn"], [(self.nt, self.smem)], [cols], b"qf_cm_a",
+                                       device_index, [self.module], [f.value])
 
     def run(self, rows, psi_src, mats_f, angles_f, coefs_f, partials_f, lam, mats_a, angles_a, coefs_a,
             coef_stride_a, partials_a, stream):
@@ -1274,7 +1288,15 @@ class TurnKernel:
         grid = (C.c_uint32 * 1)(rows << self.rows_shift)
         block = (C.c_uint32 * 1)(self.nt)
         smem = (C.c_uint32 * 1)(self.smem)
-        nat.check(lib.qf_jit_run(self.func, grid, block, smem, 1, stream, C.byref(args), C.sizeof(args)))
+        func = self.func
+        if self._slabs is not None:
+            if rows <= self._slabs.rows_max:
+                func = self._slabs.stage(rows, mats_a, a.n_mat, stream, [0])
+            else:   # more rows than the slab holds: the shared-memory variant (compiled once)
+                if self._plain is None:
+                    self._plain = TurnKernel(self.fwd, self.adj, self.device_index, cm=False)
+                func = self._plain.func
+        nat.check(lib.qf_jit_run(func, grid, block, smem, 1, stream, C.byref(args), C.sizeof(args)))
 
 
 _OPTS = [b"--gpu-architecture=sm_100a", b"-std=c++17", b"-lineinfo", b"--device-as-default-execution-space"]
@@ -1323,6 +1345,83 @@ def compile_kernel(source: str, name: str) -> bytes:
     return image
 
 
+class _SlabModules:
+    """Per-stream loaded copies of kernel modules with constant slabs (CTAU).
+
+    A module's __constant__ slab is shared by every launch of that module, so each stream (and
+    each CUDA graph, captured on its own stream) gets its own loaded copy of the modules: stream
+    order then keeps a slab write behind the launches that read the previous contents."""
+
+    def __init__(self, images, names, geo, cols, sym, device_index, base_modules, base_funcs):
+        self.images, self.names, self.geo, self.cols, self.sym = images, names, geo, cols, sym
+        self.k = [len(c) if c else 0 for c in cols]
+        self.rows_max = CM_CAP // max(self.k)
+        self.device_index = device_index
+        self.base = (list(base_modules), list(base_funcs))
+        self.inst = {}
+        self.lock = threading.Lock()
+        self.cols_t = None
+
+    def instance(self, stream):
+        key = int(stream or 0)
+        inst = self.inst.get(key)
+        if inst is not None:
+            return inst
+        import torch
+
+        lib = nat.load()
+        with self.lock:
+            inst = self.inst.get(key)
+            if inst is not None:
+                return inst
+            dev = torch.device("cuda", self.device_index)
+            if self.cols_t is None:
+                self.cols_t = [torch.tensor(c, dtype=torch.int32, device=dev) if c else None for c in self.cols]
+            if len(self.inst) >= CM_MAX_COPIES:
+                # bounded: drop the oldest copy once the device has drained its launches
+                old = self.inst.pop(next(iter(self.inst)))
+                torch.cuda.synchronize(dev)
+                for m in old[2]:
+                    if all(m is not b for b in self.base[0]):
+                        lib.qf_jit_unload(m)
+            if not any(inst_[2] is self.base[0] for inst_ in self.inst.values()):
+                mods, funcs = self.base
+            else:
+                mods, funcs = [], []
+                for img, nm, (_, smem) in zip(self.images, self.names, self.geo):
+                    mod = C.c_void_p()
+                    nat.check(lib.qf_jit_load(img, C.byref(mod)))
+                    f = C.c_void_p()
+                    nat.check(lib.qf_jit_function(mod, nm.encode(), max(smem, 48 * 1024), C.byref(f)))
+                    mods.append(mod)
+                    funcs.append(f.value)
+            slabs = []
+            for mod, c in zip(mods, self.cols):
+                if not c:
+                    slabs.append(None)
+                    continue
+                ptr, size = C.c_void_p(), C.c_size_t()
+                nat.check(lib.qf_jit_global(mod, self.sym, C.byref(ptr), C.byref(size)))
+                slabs.append((ptr.value, size.value, torch.empty(2 * CM_CAP, dtype=torch.float32, device=dev)))
+            inst = ((C.c_void_p * len(funcs))(*funcs), slabs, mods)
+            self.inst[key] = inst
+        return inst
+
+    def stage(self, rows, mats, n_mat, stream, which):
+        """Gather the launch's coefficients into the stream's slabs; returns its function array."""
+        if rows > self.rows_max:
+            raise ValueError(f"{rows} rows exceed the constant slabs ({self.rows_max} rows)")
+        funcs, slabs, _ = self.instance(stream)
+        lib = nat.load()
+        for i in which:
+            if slabs[i] is None:
+                continue
+            sym, size, staging = slabs[i]
+            nat.check(lib.qf_jit_cm_stage(mats, n_mat, rows, self.cols_t[i].data_ptr(), self.k[i],
+                                          staging.data_ptr(), sym, size, stream))
+        return funcs
+
+
 class JitProgram:
     """Compiled, loaded kernels of one planner.Program (one module per pass, compiled in parallel)."""
 
@@ -1358,12 +1457,11 @@ class JitProgram:
         self.cm = any(self.cm_k)
         self.cm_rows_max = CM_CAP // max(self.cm_k) if self.cm else 1 << 62
         self._images, self._names, self._geo = images, names, geo
-        self._cm_inst = {}
-        self._cm_lock = threading.Lock()
-        self._cm_cols_t = None
         self.n = P
         self.names = names
         self.funcs = (C.c_void_p * P)(*funcs)
+        self._slabs = _SlabModules(images, names, geo, self.cm_cols, self.cm_sym, device_index,
+                                   self.modules[:P], funcs) if self.cm else None
         self.rows_shift = prog.n - prog.L
         self.block = (C.c_uint32 * P)(*[g[0] for g in geo])
         self.smem = (C.c_uint32 * P)(*[g[1] for g in geo])
@@ -1377,72 +1475,11 @@ class JitProgram:
             nat.check(lib.qf_jit_occupancy(f, nt, smem, C.byref(occ)))
             self.resident.append(max(1, occ.value) * max(1, sms))
 
-    def _cm_instance(self, stream):
-        """(function array, [(symbol, bytes, staging)] per pass) of this stream's module copy."""
-        key = int(stream or 0)
-        inst = self._cm_inst.get(key)
-        if inst is not None:
-            return inst
-        import torch
-
-        lib = nat.load()
-        with self._cm_lock:
-            inst = self._cm_inst.get(key)
-            if inst is not None:
-                return inst
-            dev = torch.device("cuda", self.device_index)
-            if self._cm_cols_t is None:
-                self._cm_cols_t = [torch.tensor(c, dtype=torch.int32, device=dev) if c else None
-                                   for c in self.cm_cols]
-            if len(self._cm_inst) >= CM_MAX_COPIES:
-                # bounded: drop the oldest copy (after the device drained its launches)
-                old_key = next(iter(self._cm_inst))
-                old_mods = self._cm_inst.pop(old_key)[2]
-                torch.cuda.synchronize(dev)
-                for m in old_mods:
-                    if m not in self.modules[:len(self._names)]:
-                        lib.qf_jit_unload(m)
-                        self.modules.remove(m)
-            if not self._cm_inst:
-                mods = list(self.modules[:len(self._names)])
-                funcs = list(self.funcs)
-            else:
-                mods, funcs = [], []
-                for img, nm, (_, smem) in zip(self._images, self._names, self._geo):
-                    mod = C.c_void_p()
-                    nat.check(lib.qf_jit_load(img, C.byref(mod)))
-                    f = C.c_void_p()
-                    nat.check(lib.qf_jit_function(mod, nm.encode(), max(smem, 48 * 1024), C.byref(f)))
-                    self.modules.append(mod)
-                    mods.append(mod)
-                    funcs.append(f.value)
-            slabs = []
-            for mod, cols in zip(mods, self.cm_cols):
-                if not cols:
-                    slabs.append(None)
-                    continue
-                ptr, size = C.c_void_p(), C.c_size_t()
-                nat.check(lib.qf_jit_global(mod, self.cm_sym, C.byref(ptr), C.byref(size)))
-                slabs.append((ptr.value, size.value, torch.empty(2 * CM_CAP, dtype=torch.float32, device=dev)))
-            inst = ((C.c_void_p * len(funcs))(*funcs), slabs, mods)
-            self._cm_inst[key] = inst
-        return inst
-
     def _funcs_for(self, rows, mats, stream, which):
         """Function array for this launch; with constant slabs, stage passes ``which`` first."""
         if not self.cm:
             return self.funcs
-        if rows > self.cm_rows_max:
-            raise ValueError(f"{rows} rows exceed this program's constant slabs ({self.cm_rows_max} rows)")
-        funcs, slabs, _ = self._cm_instance(stream)
-        lib = nat.load()
-        for i in which:
-            if slabs[i] is None:
-                continue
-            sym, size, staging = slabs[i]
-            nat.check(lib.qf_jit_cm_stage(mats, self.prog.n_mat, rows, self._cm_cols_t[i].data_ptr(), self.cm_k[i],
-                                          staging.data_ptr(), sym, size, stream))
-        return funcs
+        return self._slabs.stage(rows, mats, self.prog.n_mat, stream, which)
 
     def remote_pass(self, g: int):
         """(function, block, smem) of the last pass with the fused swap store (compiled once per g)."""
