@@ -175,6 +175,35 @@ def test_concurrent_calls_above_jit_threshold(cuda):
         np.testing.assert_array_equal(g, wg)
 
 
+def test_constant_slab_and_shared_memory_coefficient_variants_agree(cuda, monkeypatch):
+    """Adjoint pass kernels read their rotation coefficients from per-stream __constant__ slabs
+    (jit.CTAU) when the launch's rows fit 64 KB, and from the staged shared-memory tables
+    otherwise: both variants of the same plan give the same expectations and gradients, on one
+    call that fits the slabs and on one that does not (rows above cm_rows_max)."""
+    from paper_2003_02989_b200 import jit
+    from paper_2003_02989_b200.engine import ENGINE
+
+    circ, cost = wl.qaoa_circuit(16, 2, wl.qaoa_graph(16, seed=5))
+    syms = circuit_symbols(circ)
+    theta = wl.qaoa_params(24, 2, seed=9)
+    out = {}
+    for flag in (True, False):
+        monkeypatch.setattr(jit, "CTAU", flag)
+        ENGINE._bound.clear()
+        ENGINE._plans.clear()
+        out[flag] = ops.expectation_and_gradient(circ, syms, theta, [cost])
+    np.testing.assert_allclose(out[True][0], out[False][0], atol=1e-6)
+    np.testing.assert_allclose(out[True][1], out[False][1], atol=2e-6, rtol=1e-6)
+    # a launch too tall for the slabs falls back to the shared-memory variant of the same plan
+    monkeypatch.setattr(jit, "CTAU", True)
+    monkeypatch.setattr(jit, "CM_CAP", 16)
+    ENGINE._bound.clear()
+    ENGINE._plans.clear()
+    e, g = ops.expectation_and_gradient(circ, syms, theta, [cost])
+    np.testing.assert_allclose(e, out[False][0], atol=1e-6)
+    np.testing.assert_allclose(g, out[False][1], atol=2e-6, rtol=1e-6)
+
+
 # ---------------------------------------------------------------------------
 # stochastic parameter shift vs the reference's seeded outputs
 # ---------------------------------------------------------------------------

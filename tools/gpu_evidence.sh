@@ -18,4 +18,5 @@ python tools/ncu_regions.py $OUT/a_p2_src.csv > $OUT/a_p2_regions.txt 2>&1
 timeout 2400 python tools/configs_bench.py --steps 3 > $OUT/configs.jsonl 2> $OUT/configs.err
 timeout 300 python tools/tc_bench.py > $OUT/tc_bench.json 2>&1
 tools/micro/xbar_bench > $OUT/xbar.json 2>&1
+tools/micro/ffma2_bench > $OUT/ffma2_bench.json 2>&1
 tail -3 $OUT/pytest_gpu.log; tail -2 $OUT/smoke.log; cut -c1-300 $OUT/bench.json; tail -1 $OUT/ncu_launch.log; tail -1 $OUT/ncu_full.log
