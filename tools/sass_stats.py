@@ -4,7 +4,7 @@ Generates the NVRTC sources jit.py would emit for a workload's forward/adjoint
 programs, compiles them with nvcc for sm_100a, and prints registers, spills and a
 static opcode histogram per pass (straight-line code: static ~= dynamic per thread).
 
-  python tools/sass_stats.py [qaoa|rcs|qcnn|hea] [--keep DIR]
+  python tools/sass_stats.py [qaoa|rcs|qcnn|hea] [--keep DIR] [--cm]   (--cm: constant-slab adjoint variant)
 """
 import collections
 import os
@@ -87,7 +87,7 @@ def main():
     os.makedirs(keep, exist_ok=True)
     fwd, adj = programs(name)
     for prog, tag in ((fwd, "f"), (adj, "a")):
-        srcs, names, geo = jit.generate(prog, tag)
+        srcs, names, geo = jit.generate(prog, tag, cm=("--cm" in sys.argv and prog.adjoint))
         NT = geo[0][0]
         amps = NT * (1 << prog.R)
         for s, nm in zip(srcs, names):
