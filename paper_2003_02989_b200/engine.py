@@ -8,6 +8,7 @@ is used for device allocation and host<->device copies only.
 from __future__ import annotations
 
 import ctypes as C
+import itertools
 import os
 import threading
 from collections import OrderedDict
@@ -193,6 +194,7 @@ GRAPHS = os.environ.get("QF_GRAPH", "1") not in ("0", "", "false")
 MAX_GRAPHS = int(os.environ.get("QF_MAX_GRAPHS", "2"))
 GRAPH_MIN_AMPS = 1 << 22
 _GRAPHS: OrderedDict = OrderedDict()
+_GRAPH_TOKENS = itertools.count(1)
 _GRAPH_LOCK = threading.RLock()
 
 _TORCH_OF = {
@@ -406,23 +408,37 @@ class Bound:
             if hit is not None and hit[0] is self:
                 _GRAPHS.move_to_end(key)
             else:
+                from . import jit as _jit
+
+                if hit is not None:                    # a dead Bound's graph under a reused id
+                    stale = _GRAPHS.pop(key)
+                    torch.cuda.synchronize(dev)
+                    stale[1].reset()
+                    _jit.release_slab_owner(stale[4])
                 static = torch.empty(theta.shape, dtype=torch.float32, device=dev)
                 static.copy_(theta)
+
                 side = torch.cuda.Stream(dev)
                 side.wait_stream(cur)
-                with torch.cuda.stream(side):      # warm-up: NVRTC compiles, allocator sizing
-                    self._execute(static, want_grad=want_grad, want_expect=want_expect)
-                cur.wait_stream(side)
                 graph = torch.cuda.CUDAGraph()
-                # captured on the warm-up stream: its per-stream kernel modules (constant slabs,
-                # jit.CTAU) are loaded already and belong to this graph alone
-                with torch.cuda.graph(graph, stream=side, capture_error_mode="thread_local"):
-                    out = self._execute(static, want_grad=want_grad, want_expect=want_expect)
-                hit = (self, graph, static, out)
+                # the graph owns its copies of the kernel modules with constant slabs (jit.CTAU):
+                # loaded by the warm-up, written only by this graph's own replays, pinned until
+                # the graph leaves the cache
+                token = next(_GRAPH_TOKENS)
+                with _jit.slab_owner(token):
+                    with torch.cuda.stream(side):      # warm-up: NVRTC compiles, allocator sizing
+                        self._execute(static, want_grad=want_grad, want_expect=want_expect)
+                    cur.wait_stream(side)
+                    with torch.cuda.graph(graph, stream=side, capture_error_mode="thread_local"):
+                        out = self._execute(static, want_grad=want_grad, want_expect=want_expect)
+                hit = (self, graph, static, out, token)
                 _GRAPHS[key] = hit
                 while len(_GRAPHS) > MAX_GRAPHS:       # each graph holds its buffers (checkpoints)
-                    _GRAPHS.popitem(last=False)
-            _, graph, static, out = hit
+                    _, gone = _GRAPHS.popitem(last=False)
+                    torch.cuda.synchronize(dev)
+                    gone[1].reset()                    # the graph goes before its kernel modules
+                    _jit.release_slab_owner(gone[4])
+            _, graph, static, out, _ = hit
             static.copy_(theta, non_blocking=True)
             graph.replay()
             # outputs are copied before the lock is released: the next replay on this stream

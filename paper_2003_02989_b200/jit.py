@@ -17,6 +17,7 @@ import ctypes as C
 import hashlib
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -1345,12 +1346,40 @@ def compile_kernel(source: str, name: str) -> bytes:
     return image
 
 
+# Owner of the slab copies a thread's launches use: None = the launch stream; a CUDA graph being
+# captured sets its own token (slab_owner), so the graph's kernel nodes point into module copies
+# no stream -- and no other graph -- ever writes, pinned until release_slab_owner(token).
+_SLAB_OWNER = threading.local()
+_SLAB_SETS = weakref.WeakSet()
+
+
+class slab_owner:
+    """Context: this thread's constant-slab launches use module copies owned by ``token``."""
+
+    def __init__(self, token):
+        self.token = token
+
+    def __enter__(self):
+        self.prev = getattr(_SLAB_OWNER, "token", None)
+        _SLAB_OWNER.token = self.token
+
+    def __exit__(self, *exc):
+        _SLAB_OWNER.token = self.prev
+
+
+def release_slab_owner(token) -> None:
+    """Unload the module copies pinned for ``token`` (its graph is gone)."""
+    for sm in list(_SLAB_SETS):
+        sm.release(("owner", token))
+
+
 class _SlabModules:
     """Per-stream loaded copies of kernel modules with constant slabs (CTAU).
 
     A module's __constant__ slab is shared by every launch of that module, so each stream (and
-    each CUDA graph, captured on its own stream) gets its own loaded copy of the modules: stream
-    order then keeps a slab write behind the launches that read the previous contents."""
+    each CUDA graph, through slab_owner) gets its own loaded copy of the modules: stream order
+    then keeps a slab write behind the launches that read the previous contents.  Stream copies
+    are bounded (oldest dropped after a device sync); graph-owned copies stay until released."""
 
     def __init__(self, images, names, geo, cols, sym, device_index, base_modules, base_funcs):
         self.images, self.names, self.geo, self.cols, self.sym = images, names, geo, cols, sym
@@ -1361,9 +1390,24 @@ class _SlabModules:
         self.inst = {}
         self.lock = threading.Lock()
         self.cols_t = None
+        _SLAB_SETS.add(self)
+
+    def release(self, key):
+        import torch
+
+        with self.lock:
+            old = self.inst.pop(key, None)
+            if old is None:
+                return
+            torch.cuda.synchronize(torch.device("cuda", self.device_index))
+            lib = nat.load()
+            for m in old[2]:
+                if all(m is not b for b in self.base[0]):
+                    lib.qf_jit_unload(m)
 
     def instance(self, stream):
-        key = int(stream or 0)
+        token = getattr(_SLAB_OWNER, "token", None)
+        key = ("owner", token) if token is not None else int(stream or 0)
         inst = self.inst.get(key)
         if inst is not None:
             return inst
@@ -1377,9 +1421,10 @@ class _SlabModules:
             dev = torch.device("cuda", self.device_index)
             if self.cols_t is None:
                 self.cols_t = [torch.tensor(c, dtype=torch.int32, device=dev) if c else None for c in self.cols]
-            if len(self.inst) >= CM_MAX_COPIES:
-                # bounded: drop the oldest copy once the device has drained its launches
-                old = self.inst.pop(next(iter(self.inst)))
+            streams = [k for k in self.inst if not isinstance(k, tuple)]
+            if len(streams) >= CM_MAX_COPIES:
+                # bounded: drop the oldest stream copy once the device has drained its launches
+                old = self.inst.pop(streams[0])
                 torch.cuda.synchronize(dev)
                 for m in old[2]:
                     if all(m is not b for b in self.base[0]):

@@ -204,6 +204,34 @@ def test_constant_slab_and_shared_memory_coefficient_variants_agree(cuda, monkey
     np.testing.assert_allclose(g, out[False][1], atol=2e-6, rtol=1e-6)
 
 
+def test_graph_replays_own_their_constant_slabs(cuda, monkeypatch):
+    """CUDA-graph replays of one bound (>= 2^22 amplitudes, device-resident angles) re-stage the
+    rotation coefficients of every replay into module copies the graph owns: alternating angle
+    sets and row counts -- with a one-graph cache, so every switch evicts a graph and unloads
+    its module copies -- give the same results as the ungraphed launch sequence."""
+    import torch
+
+    from paper_2003_02989_b200 import engine as eng
+
+    circ, cost = wl.qaoa_circuit(18, 1, wl.qaoa_graph(18, seed=3))
+    syms = circuit_symbols(circ)
+    thetas = [torch.as_tensor(wl.qaoa_params(b, 1, seed=40 + i)).cuda() for i, b in enumerate((16, 20, 16))]
+    monkeypatch.setattr(eng, "GRAPHS", False)
+    want = [ops.expectation_and_gradient(circ, syms, t, [cost]) for t in thetas]
+    monkeypatch.setattr(eng, "GRAPHS", True)
+    monkeypatch.setattr(eng, "MAX_GRAPHS", 1)
+    for rep in range(2):
+        for t, (we, wg) in zip(thetas, want):
+            e, g = ops.expectation_and_gradient(circ, syms, t, [cost])
+            assert torch.equal(e, we) and torch.equal(g, wg), rep
+    assert len(eng._GRAPHS) == 1
+    # same shape, new angles: one graph, replayed
+    monkeypatch.setattr(eng, "MAX_GRAPHS", 2)
+    for i in (0, 2, 0, 2):
+        e, g = ops.expectation_and_gradient(circ, syms, thetas[i], [cost])
+        assert torch.equal(e, want[i][0]) and torch.equal(g, want[i][1])
+
+
 # ---------------------------------------------------------------------------
 # stochastic parameter shift vs the reference's seeded outputs
 # ---------------------------------------------------------------------------
